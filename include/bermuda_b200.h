@@ -1,0 +1,193 @@
+/*
+ * bermuda_b200.h -- C ABI of the B200 nested-Monte-Carlo engine
+ * (libbermuda_b200.so, built from paper_0805_1827_b200/csrc/).
+ *
+ * Drop-in boundary for the reference package `bermuda` (arXiv 0805.1827):
+ * every entry point replaces one function of the reference's duck-typed
+ * kernel-backend module (pkg/src/bermuda/_kernels/core_backend.py:12-58,
+ * numpy_backend.py:19-190) or one phase body of its builders, and is cited
+ * below.  Plain C types only: no torch, no numpy.
+ *
+ * Buffers.  Every array argument may be HOST memory (pageable or pinned) or
+ * DEVICE memory of the context's GPU; the library inspects each pointer.
+ * Host inputs are staged to HBM and host outputs copied back before the call
+ * returns.  When every output of a call is device memory the call is
+ * stream-ordered and returns without synchronising (see brm_ctx_set_stream).
+ *
+ * Errors.  Functions return BRM_OK (0) or a status; brm_last_error() gives
+ * the message (thread-local).  The Python shim maps BRM_EINVAL to ValueError
+ * (the reference raises ValueError for a start date with no remaining
+ * exercise dates, _core.pyx:406-407, 445-446, 524-525) and BRM_ENOMEM to
+ * MemoryError (_core.pyx:418-421).
+ *
+ * Precision modes (per context).  BRM_MODE_PARITY reproduces the reference
+ * pipeline: Philox4x32-10 words, 53-bit uniforms and AS241 normals in fp64
+ * with the reference draw indexing (_core.pyx:4-7) and no FMA contraction,
+ * so draws are the reference's draws and per-path values agree to the last
+ * ulp of exp().  BRM_MODE_FAST steps paths in fp32 with Box-Muller normals
+ * from the same Philox counter space and accumulates in fp64 (BASELINE.json
+ * configs 3-4); it agrees with the reference statistically only.
+ */
+#ifndef BERMUDA_B200_H
+#define BERMUDA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define BRM_ABI_VERSION 1
+
+enum brm_status {
+    BRM_OK = 0,
+    BRM_EINVAL = 1,   /* invalid argument            -> ValueError   */
+    BRM_ENOMEM = 2,   /* allocation failure          -> MemoryError  */
+    BRM_ECUDA = 3,    /* CUDA runtime / launch error -> RuntimeError */
+    BRM_ENODEV = 4    /* no usable sm_100 device     -> RuntimeError */
+};
+
+enum brm_mode { BRM_MODE_PARITY = 0, BRM_MODE_FAST = 1 };
+
+/* Payoff codes: 0-2 are the reference's (packs.py:33-35); 3-4 are the
+ * BASELINE.json configs 2 and 4 the reference cannot express. */
+enum brm_payoff {
+    BRM_PAY_MAXCALL = 0, BRM_PAY_PUT = 1, BRM_PAY_CALL = 2,
+    BRM_PAY_GEOPUT = 3, BRM_PAY_BASKETPUT = 4
+};
+
+/* Rule kinds (packs.py:28-31). */
+enum brm_rule_kind { BRM_RULE_EUROPEAN = 0, BRM_RULE_IMMEDIATE = 1, BRM_RULE_IZ = 2, BRM_RULE_CMC = 3 };
+
+/* Stream phases (rng.py:55-61). */
+enum brm_phase { BRM_PHASE_GLP = 0, BRM_PHASE_IZ_CALC = 1, BRM_PHASE_CMC_CALC = 2, BRM_PHASE_PRICING = 3 };
+
+/* Market pack (packs.py:44-71).  Arrays are host or device. */
+typedef struct brm_market_desc {
+    int32_t d, n_dates, payoff_kind;
+    double strike;
+    const double *step_mu;     /* [d]          log drift per exercise step  */
+    const double *step_vol;    /* [d]          sigma*sqrt(dt)                */
+    const double *chol;        /* [d*d]        correlation factor, row-major */
+    const double *disc_steps;  /* [n_dates+1]  exp(-r*k*dt)                  */
+    const double *s0;          /* [d]                                        */
+} brm_market_desc;
+
+/* Rule pack (packs.py:100-193).  iz_space 0 is the reference's price-space
+ * surfaces of the argmax asset (_core.pyx:227-268); 1 is a log-space surface
+ * of the last asset over the other log prices (geometric put, config 2). */
+typedef struct brm_rule_desc {
+    int32_t kind, call_like, imm_date;
+    int32_t nbasis, iz_space;
+    const double *iz_coeffs;   /* [(n_dates+1)*d*nbasis] */
+    const double *iz_lo, *iz_hi; /* [d-1] clamp box (log box when iz_space 1) */
+    int32_t n_stumps;
+    const int32_t *cmc_starts, *cmc_counts; /* [n_dates+1] */
+    const int32_t *cmc_feat;   /* [n_stumps]; index d = derived feature */
+    const double *cmc_thr, *cmc_pol, *cmc_alpha; /* [n_stumps] */
+    const double *cmc_intercept; /* [n_dates+1] */
+} brm_rule_desc;
+
+typedef struct brm_ctx brm_ctx;
+
+int brm_abi_version(void);
+const char *brm_last_error(void);
+int brm_device_count(int32_t *count);
+
+/* Context = device-resident copy of one (MarketPack, RulePack) pair; replaces
+ * the reference's cached _CtxHolder (core_backend.py:23-33, _core.pyx:334-378). */
+int brm_ctx_create(const brm_market_desc *market, const brm_rule_desc *rule, int32_t device, int32_t mode,
+                   brm_ctx **out);
+int brm_ctx_destroy(brm_ctx *ctx);
+/* Launch on a caller-owned cudaStream_t (e.g. torch's current stream); NULL restores the context's own. */
+int brm_ctx_set_stream(brm_ctx *ctx, void *cuda_stream);
+/* Fixed-input mode: draw index i of every stream reads normals[i - base]
+ * instead of the generator (north star "identical host-supplied normal
+ * draws").  normals == NULL returns to the generator. */
+int brm_ctx_supply_normals(brm_ctx *ctx, const double *normals, uint64_t base, uint64_t count);
+
+/* ---- RNG (rng.py:79-216; _core.pyx:149-181) ---------------------------- */
+int brm_derive_words(uint64_t seed, uint32_t phase, uint64_t item, uint64_t date, uint64_t *key64,
+                     uint64_t *stream64);
+int brm_raw_uint64(int32_t device, uint64_t key64, uint64_t stream64, uint64_t start, int64_t count,
+                   uint64_t *out);
+int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t start, int64_t count,
+                double *out);
+
+/* ---- Path walker ------------------------------------------------------- */
+/* stopped_sums (core_backend.py:36-41, _core.pyx:402-430). */
+int brm_stopped_sums(brm_ctx *ctx, const double *start_values, int32_t m_start, int64_t n_paths,
+                     uint64_t key64, uint64_t stream64, uint64_t draw_base, double *sum, double *sumsq);
+/* Per-path discounted values and stop dates (0 = never exercised) of the
+ * same paths stopped_sums folds: path p starts at draw_base + p*per_path. */
+int brm_path_values(brm_ctx *ctx, const double *start_values, int32_t m_start, int64_t n_paths,
+                    uint64_t key64, uint64_t stream64, uint64_t draw_base, double *values,
+                    int32_t *stop_dates);
+/* Exercise decision of the context's rule for n states at date m
+ * (pricer.py:104-133 iz_exercise_rule / cmc_exercise_rule). */
+int brm_decisions(brm_ctx *ctx, const double *states, int64_t n, int32_t m, int32_t *out);
+
+/* Final pricing: blocks [block_lo, block_hi) of PATH_BLOCK=4096 paths, block
+ * b on StreamKey(seed, PRICING, b) from s0 at date 0; out_stats[b-block_lo] =
+ * (count, sum, sumsq)  (pricer.py:154-164). */
+int brm_price_blocks(brm_ctx *ctx, int64_t n_paths, uint64_t seed, int64_t block_lo, int64_t block_hi,
+                     double *out_stats);
+
+/* cmc_labels (core_backend.py:52-58, _core.pyx:515-550): beta_i =
+ * payoff(x_i) - mean of n_label stopped paths from x_i at date m on stream
+ * (keys[i], streams[i]) from draw_base.  keys == NULL derives them on the
+ * device as StreamKey(seed, CMC_CALC, item_lo + i, m) (boundary_cmc.py:220). */
+int brm_cmc_labels(brm_ctx *ctx, const double *points, int64_t n, int32_t m, int32_t n_label,
+                   const uint64_t *keys, const uint64_t *streams, uint64_t seed, int64_t item_lo,
+                   uint64_t draw_base, double *out_beta);
+
+/* Training points at date m for items [item_lo, item_lo+n) on
+ * StreamKey(seed, CMC_CALC, item, m).  mode 0 = the reference sampler
+ * (terminal draw + Brownian bridge, boundary_cmc.py:164-177, labels then
+ * start at draw 2d); mode 1 = forward from S0 over dates 1..m (labels start
+ * at draw m*d).  bridge holds 4*d+1 host-computed scalars:
+ * [drift_T(d), sig_sqrt_T(d), log_s0(d), bridge_sd(d), lam]. */
+int brm_sample_points(brm_ctx *ctx, int32_t mode, int32_t m, uint64_t seed, int64_t item_lo, int64_t n,
+                      const double *bridge, double *out_points);
+
+/* ---- I&Z probes (_core.pyx:433-512; BASELINE bisection) ----------------- */
+/* n probes; seeds [n*(d-1)] (row-major), assets [n]; keys NULL derives
+ * StreamKey(seed, IZ_CALC, item_lo + i, m) (boundary_iz.py:288).
+ * solver 0: fixed point u <- K +/- C(u) from K, fresh draws per iteration,
+ *           armed |step| < eps stop, mean of the last avg_window iterates.
+ * solver 1: bisection of payoff - C on [lo, hi] to width tol with common
+ *           random numbers.  Levels are prices of the probed asset. */
+int brm_iz_solve(brm_ctx *ctx, int32_t solver, const double *seeds, const int32_t *assets, int64_t n,
+                 int32_t m, int32_t n_inner, double eps, int32_t max_iter, int32_t avg_window, double lo,
+                 double hi, double tol, const uint64_t *keys, const uint64_t *streams, uint64_t seed,
+                 int64_t item_lo, double *out_level, int32_t *out_iterations, int32_t *out_converged);
+
+/* ---- AdaBoost stumps (boosting.py:126-206) ------------------------------ */
+/* xs [n*F] row-major features, betas [n] (y = +1 iff beta > 0).  mode
+ * BRM_MODE_PARITY replays numpy's summation orders (sequential cumsum,
+ * pairwise sum) and the reference tie rules; BRM_MODE_FAST uses exact
+ * fixed-point weight scans.  Outputs sized [rounds]; *out_count stumps
+ * picked; *out_intercept the ensemble intercept. */
+int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, const double *betas, int64_t n,
+                     int32_t F, int32_t rounds, int32_t *out_feat, double *out_thr, double *out_pol,
+                     double *out_alpha, int32_t *out_count, double *out_intercept);
+
+/* ---- Quadratic boundary regression (boundary_iz.py:250-276) ------------- */
+/* Least squares over the design [n*nb] (row-major), fp64 Householder QR on
+ * the device; rank-deficient designs fall back to the cross-term-free basis
+ * (zeros in dropped columns).  *out_rank_deficient set to 1 on fallback. */
+int brm_lstsq(int32_t device, const double *design, const double *levels, int64_t n, int32_t nb,
+              int32_t k_coords, double *out_coeffs, int32_t *out_rank_deficient);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BERMUDA_B200_H */

@@ -1,0 +1,691 @@
+// brm_boost.cu -- AdaBoost decision stumps (boosting.py:126-206) and the
+// quadratic boundary regression (boundary_iz.py:250-276) on the device.
+//
+// AdaBoost runs as ONE cooperative kernel for the whole ensemble: a CTA per
+// feature.  Each column is sorted once per fit (stable radix sort, the
+// reference re-sorts every round, boosting.py:143); per round
+//   every CTA  : total = sum(w) in numpy's pairwise order (redundantly: no sync)
+//   CTA f      : sequential prefix sums of positive / negative weights in the
+//                sorted order (numpy cumsum order), then a parallel scan of
+//                the split points for the interleaved first-hit argmin
+//   grid sync  ; every CTA picks the same winner (lowest feature, then lowest
+//                threshold, then +1 polarity at exact ties), forms alpha
+//   all CTAs   : w *= exp(-alpha y pred) on a slice; grid sync; w /= sum(w)
+//                (pairwise order); grid sync
+// Products and sums are separately rounded fp64 like numpy's, so the split
+// search reproduces the reference bit for bit on identical inputs; alpha and
+// exp(+-alpha) come from CUDA's log/exp (<= 1 ulp from numpy's).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/bermuda_b200.h"
+#include "brm_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace brm {
+
+constexpr int kBoostThreads = 256;
+constexpr int kTile = 2048;
+constexpr int kPwBlock = 128;  // numpy PW_BLOCKSIZE
+
+// numpy pairwise_sum leaf (n <= 128): 8 strided accumulators, fixed combine,
+// then the tail added in order (n < 8: plain sequential from 0).
+__device__ double pw_leaf(const double *a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// Leaves of numpy's recursion over n elements, left to right (host side).
+static void pw_leaves(int64_t off, int64_t n, std::vector<int2> &out) {
+  if (n <= kPwBlock) {
+    out.push_back(make_int2((int)off, (int)n));
+    return;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  pw_leaves(off, n2, out);
+  pw_leaves(off + n2, n - n2, out);
+}
+
+// Combine leaf sums along the same recursion (thread-local, iterative).
+__device__ double pw_combine(const double *leaf, int n) {
+  // explicit stack of (len, state); a node of len <= 128 consumes one leaf
+  struct Frame {
+    int len;
+    int stage;
+    double left;
+  };
+  Frame st[48];
+  int sp = 0, next_leaf = 0;
+  double ret = 0.0;
+  st[sp++] = Frame{n, 0, 0.0};
+  while (sp > 0) {
+    Frame &f = st[sp - 1];
+    if (f.len <= kPwBlock) {
+      ret = leaf[next_leaf++];
+      --sp;
+      continue;
+    }
+    int n2 = f.len / 2;
+    n2 -= n2 % 8;
+    if (f.stage == 0) {
+      f.stage = 1;
+      st[sp++] = Frame{n2, 0, 0.0};
+    } else if (f.stage == 1) {
+      f.left = ret;
+      f.stage = 2;
+      st[sp++] = Frame{f.len - n2, 0, 0.0};
+    } else {
+      ret = __dadd_rn(f.left, ret);
+      --sp;
+    }
+  }
+  return ret;
+}
+
+// numpy pairwise sum of a[0..n) by one thread (rare paths only).
+__device__ double pw_serial(const double *a, int n) {
+  struct Frame {
+    int off, len, stage;
+    double left;
+  };
+  Frame st[48];
+  int sp = 0;
+  double ret = 0.0;
+  st[sp++] = Frame{0, n, 0, 0.0};
+  while (sp > 0) {
+    Frame &f = st[sp - 1];
+    if (f.len <= kPwBlock) {
+      ret = pw_leaf(a + f.off, f.len);
+      --sp;
+      continue;
+    }
+    int n2 = f.len / 2;
+    n2 -= n2 % 8;
+    if (f.stage == 0) {
+      f.stage = 1;
+      st[sp++] = Frame{f.off, n2, 0, 0.0};
+    } else if (f.stage == 1) {
+      f.left = ret;
+      f.stage = 2;
+      st[sp++] = Frame{f.off + n2, f.len - n2, 0, 0.0};
+    } else {
+      ret = __dadd_rn(f.left, ret);
+      --sp;
+    }
+  }
+  return ret;
+}
+
+// CTA-wide numpy-order sum of a[0..n); result broadcast to all threads.
+__device__ double cta_pairwise(const double *a, int n, const int2 *leaves, int n_leaves, double *s_leaf,
+                               double *s_out) {
+  for (int l = threadIdx.x; l < n_leaves; l += blockDim.x) s_leaf[l] = pw_leaf(a + leaves[l].x, leaves[l].y);
+  __syncthreads();
+  if (threadIdx.x == 0) *s_out = n == 0 ? 0.0 : pw_combine(s_leaf, n);
+  __syncthreads();
+  const double r = *s_out;
+  __syncthreads();
+  return r;
+}
+
+struct BoostParams {
+  int n, F, rounds;
+  const double *xs;        // [n][F]
+  const double *xsorted;   // [F][n]
+  const int *order;        // [F][n]
+  const double *y;         // [n] +-1
+  double *w;               // [n]
+  double *pcum, *ncum;     // [F][n]
+  const int2 *leaves;
+  int n_leaves;
+  double *feat_err;        // [F]
+  int *feat_pos;           // [F] 2*i + (pol == -1)
+  double *wsub;            // [F][n] per-CTA scratch for the constant-stump sums
+  int *out_feat;
+  double *out_thr, *out_pol, *out_alpha;
+  int *out_count;
+};
+
+struct Cand {
+  double err;
+  int key;  // 2*i + (minus polarity)
+};
+
+__device__ __forceinline__ bool cand_less(const Cand &a, const Cand &b) {
+  return a.err < b.err || (a.err == b.err && a.key < b.key);
+}
+
+__global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *s_leaf = reinterpret_cast<double *>(smem_raw);        // [n_leaves]
+  double *s_w = s_leaf + P.n_leaves;                            // [kTile] sorted weights
+  double *s_pc = s_w + kTile;                                   // [kTile]
+  double *s_nc = s_pc + kTile;                                  // [kTile]
+  unsigned char *s_pos = reinterpret_cast<unsigned char *>(s_nc + kTile);  // [kTile]
+  __shared__ double s_sum;
+  __shared__ Cand s_cand[kBoostThreads / 32];
+  __shared__ int s_stop;
+  __shared__ double s_alpha, s_thr, s_pol;
+  __shared__ int s_feat;
+
+  const int n = P.n, F = P.F;
+  const int f = blockIdx.x;
+  const int slice = (n + gridDim.x - 1) / gridDim.x;
+  const int w_lo = blockIdx.x * slice, w_hi = min(w_lo + slice, n);
+  int count = 0;
+
+  for (int round = 0; round < P.rounds; ++round) {
+    // ---- split search on feature f -------------------------------------
+    const double total = cta_pairwise(P.w, n, P.leaves, P.n_leaves, s_leaf, &s_sum);
+    if (f < F) {
+      const int *ord = P.order + (size_t)f * n;
+      double *pc = P.pcum + (size_t)f * n;
+      double *nc = P.ncum + (size_t)f * n;
+      double pacc = 0.0, nacc = 0.0;
+      for (int t0 = 0; t0 < n; t0 += kTile) {
+        const int tn = min(kTile, n - t0);
+        for (int j = threadIdx.x; j < tn; j += blockDim.x) {
+          const int idx = ord[t0 + j];
+          s_w[j] = P.w[idx];
+          s_pos[j] = P.y[idx] > 0.0;
+        }
+        __syncthreads();
+        // np.cumsum(where(y>0, w, 0)): adding 0.0 never changes a partial sum,
+        // so the positive and negative prefix chains run independently.
+        if (threadIdx.x == 0) {
+          for (int j = 0; j < tn; ++j) {
+            if (s_pos[j]) pacc = __dadd_rn(pacc, s_w[j]);
+            s_pc[j] = pacc;
+          }
+        } else if (threadIdx.x == 32) {
+          for (int j = 0; j < tn; ++j) {
+            if (!s_pos[j]) nacc = __dadd_rn(nacc, s_w[j]);
+            s_nc[j] = nacc;
+          }
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < tn; j += blockDim.x) {
+          pc[t0 + j] = s_pc[j];
+          nc[t0 + j] = s_nc[j];
+        }
+        __syncthreads();
+      }
+      __threadfence_block();
+      const double *xf = P.xsorted + (size_t)f * n;
+      const double tot_neg = nc[n - 1];
+      Cand best{__longlong_as_double(0x7ff0000000000000LL), 0x7fffffff};
+      for (int i = threadIdx.x; i < n - 1; i += blockDim.x) {
+        if (!(__dsub_rn(xf[i + 1], xf[i]) > 0.0)) continue;
+        const double ep = __dadd_rn(pc[i], __dsub_rn(tot_neg, nc[i]));
+        const double em = __dsub_rn(total, ep);
+        const Cand a{ep, 2 * i}, b{em, 2 * i + 1};
+        if (cand_less(a, best)) best = a;
+        if (cand_less(b, best)) best = b;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        Cand o;
+        o.err = __shfl_down_sync(0xffffffffu, best.err, off);
+        o.key = __shfl_down_sync(0xffffffffu, best.key, off);
+        if (cand_less(o, best)) best = o;
+      }
+      if ((threadIdx.x & 31) == 0) s_cand[threadIdx.x >> 5] = best;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int wi = 1; wi < (int)blockDim.x / 32; ++wi)
+          if (cand_less(s_cand[wi], best)) best = s_cand[wi];
+        P.feat_err[f] = best.err;
+        P.feat_pos[f] = best.key;
+      }
+    }
+    grid.sync();
+    // ---- pick the winner (every CTA, same answer) ------------------------
+    if (threadIdx.x == 0) {
+      double be = __longlong_as_double(0x7ff0000000000000LL);
+      int bf = -1, bk = 0;
+      for (int g = 0; g < F; ++g)
+        if (P.feat_pos[g] != 0x7fffffff && P.feat_err[g] < be) {
+          be = P.feat_err[g];
+          bf = g;
+          bk = P.feat_pos[g];
+        }
+      double thr, pol, err;
+      int feat;
+      if (bf < 0) {
+        // every feature constant: weighted majority constant stump
+        feat = 0;
+        thr = __longlong_as_double(0xfff0000000000000LL);
+        s_stop = 2;  // resolved below by the whole CTA
+        pol = 0.0;
+        err = 0.0;
+      } else {
+        feat = bf;
+        const int i = bk >> 1;
+        const double *xf = P.xsorted + (size_t)bf * n;
+        thr = __dmul_rn(0.5, __dadd_rn(xf[i], xf[i + 1]));
+        pol = (bk & 1) ? -1.0 : 1.0;
+        err = be;
+        s_stop = 0;
+      }
+      s_feat = feat;
+      s_thr = thr;
+      s_pol = pol;
+      s_alpha = err;  // holds err until alpha is formed
+    }
+    __syncthreads();
+    if (s_stop == 2) {
+      // every feature constant (boosting.py:166-170): pol = +1 iff sum(w*y) >= 0,
+      // err = sum(w[y != pol]), both in numpy's pairwise order; per-CTA scratch
+      double *ws = P.wsub + (size_t)blockIdx.x * n;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) ws[i] = __dmul_rn(P.w[i], P.y[i]);
+      __syncthreads();
+      const double swy = cta_pairwise(ws, n, P.leaves, P.n_leaves, s_leaf, &s_sum);
+      const double pol = swy >= 0.0 ? 1.0 : -1.0;
+      if (threadIdx.x == 0) {
+        int k = 0;
+        for (int i = 0; i < n; ++i)
+          if (P.y[i] != pol) ws[k++] = P.w[i];
+        s_feat = 0;
+        s_pol = pol;
+        s_alpha = pw_serial(ws, k);
+        s_stop = 0;
+      }
+      __syncthreads();
+    }
+    // alpha = 0.5 * log((1 - err) / max(err, 1e-10)); stop rules of fit_ensemble
+    if (threadIdx.x == 0) {
+      const double err = s_alpha;
+      if (err >= 0.5) {
+        s_stop = 1;
+      } else {
+        const double a = __dmul_rn(0.5, log(__ddiv_rn(__dsub_rn(1.0, err), err > 1e-10 ? err : 1e-10)));
+        s_alpha = a;
+        if (blockIdx.x == 0) {
+          P.out_feat[count] = s_feat;
+          P.out_thr[count] = s_thr;
+          P.out_pol[count] = s_pol;
+          P.out_alpha[count] = a;
+        }
+        s_stop = err <= 0.0 ? 3 : 0;
+      }
+    }
+    __syncthreads();
+    if (s_stop == 1) break;
+    ++count;
+    if (s_stop == 3 || round + 1 == P.rounds) break;
+    // ---- reweight: w *= exp(-alpha * y * pred); then w /= sum(w) -----------
+    {
+      const double a = s_alpha, thr = s_thr, pol = s_pol;
+      const int feat = s_feat;
+      const double e_agree = exp(-a), e_miss = exp(a);
+      for (int i = w_lo + threadIdx.x; i < w_hi; i += blockDim.x) {
+        const double pred = P.xs[(size_t)i * F + feat] > thr ? pol : -pol;
+        P.w[i] = __dmul_rn(P.w[i], (P.y[i] * pred > 0.0) ? e_agree : e_miss);
+      }
+    }
+    grid.sync();
+    {
+      const double s = cta_pairwise(P.w, n, P.leaves, P.n_leaves, s_leaf, &s_sum);
+      for (int i = w_lo + threadIdx.x; i < w_hi; i += blockDim.x) P.w[i] = __ddiv_rn(P.w[i], s);
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *P.out_count = count;
+}
+
+__global__ void transpose_cols(const double *xs, int n, int F, double *xt, int *iota) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * F) return;
+  const int r = (int)(i / F), c = (int)(i % F);
+  xt[(size_t)c * n + r] = __dadd_rn(xs[i], 0.0);  // -0.0 -> +0.0: numpy sorts them as equal
+  if (c == 0) iota[r] = r;
+}
+
+__global__ void labels_from_betas(const double *betas, int n, double *y, int *npos) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool pos = betas[i] > 0.0;
+  y[i] = pos ? 1.0 : -1.0;
+  if (pos) atomicAdd(npos, 1);
+}
+
+__global__ void fill_value(double *w, int n, double v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) w[i] = v;
+}
+
+// --------------------------------------------------------------- lstsq ----
+// Householder QR with column pivoting in one CTA (fp64).  Returns rank.
+constexpr int kLsMaxN = 4096, kLsMaxB = 64;
+
+__global__ void lstsq_kernel(const double *design, const double *levels, int n, int nb, const int *cols, int ncols,
+                             double *coeffs, int *rank_out) {
+  extern __shared__ double sm[];
+  double *A = sm;                       // [ncols][n] column-major
+  double *b = A + (size_t)ncols * n;    // [n]
+  __shared__ double s_norm[kLsMaxB];
+  __shared__ int s_perm[kLsMaxB];
+  __shared__ double s_tau, s_beta, s_r00;
+  __shared__ int s_rank;
+  for (int i = threadIdx.x; i < n * ncols; i += blockDim.x) {
+    const int c = i / n, r = i % n;
+    A[i] = design[(size_t)r * nb + cols[c]];
+  }
+  for (int r = threadIdx.x; r < n; r += blockDim.x) b[r] = levels[r];
+  if (threadIdx.x < ncols) s_perm[threadIdx.x] = threadIdx.x;
+  if (threadIdx.x == 0) s_rank = 0;
+  __syncthreads();
+  const int kmax = min(n, ncols);
+  for (int k = 0; k < kmax; ++k) {
+    // column norms of the trailing block, pick the largest
+    for (int c = k + (threadIdx.x >> 5); c < ncols; c += blockDim.x >> 5) {
+      double s = 0.0;
+      for (int r = k + (threadIdx.x & 31); r < n; r += 32) s += A[(size_t)c * n + r] * A[(size_t)c * n + r];
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+      if ((threadIdx.x & 31) == 0) s_norm[c] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int best = k;
+      for (int c = k + 1; c < ncols; ++c)
+        if (s_norm[c] > s_norm[best]) best = c;
+      s_beta = best;
+    }
+    __syncthreads();
+    const int piv = (int)s_beta;
+    if (piv != k) {
+      for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        const double t = A[(size_t)k * n + r];
+        A[(size_t)k * n + r] = A[(size_t)piv * n + r];
+        A[(size_t)piv * n + r] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = s_perm[k];
+        s_perm[k] = s_perm[piv];
+        s_perm[piv] = t;
+      }
+    }
+    __syncthreads();
+    // Householder vector for column k
+    if (threadIdx.x == 0) {
+      double nrm = 0.0;
+      for (int r = k; r < n; ++r) nrm += A[(size_t)k * n + r] * A[(size_t)k * n + r];
+      nrm = sqrt(nrm);
+      const double x0 = A[(size_t)k * n + k];
+      const double alpha = x0 >= 0.0 ? -nrm : nrm;
+      if (k == 0) s_r00 = fabs(alpha);
+      const double tol = (double)max(n, ncols) * 2.220446049250313e-16 * s_r00;
+      if (!(fabs(alpha) > tol) || nrm == 0.0) {
+        s_tau = 0.0;
+      } else {
+        s_rank = k + 1;
+        const double v0 = x0 - alpha;
+        A[(size_t)k * n + k] = alpha;
+        for (int r = k + 1; r < n; ++r) A[(size_t)k * n + r] /= v0;
+        s_tau = -v0 / alpha;  // H = I - tau v v^T with v = [1, A[k+1..n)]
+      }
+    }
+    __syncthreads();
+    const double tau = s_tau;
+    if (tau == 0.0) break;
+    // apply H to trailing columns and b
+    for (int c = k + 1 + (threadIdx.x >> 5); c <= ncols; c += blockDim.x >> 5) {
+      double *col = c < ncols ? A + (size_t)c * n : b;
+      double s = 0.0;
+      for (int r = k + (threadIdx.x & 31); r < n; r += 32) s += (r == k ? 1.0 : A[(size_t)k * n + r]) * col[r];
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+      s = __shfl_sync(0xffffffffu, s, 0) * tau;
+      for (int r = k + (threadIdx.x & 31); r < n; r += 32) col[r] -= s * (r == k ? 1.0 : A[(size_t)k * n + r]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int rk = s_rank;
+    *rank_out = rk;
+    double x[kLsMaxB];
+    for (int i = rk - 1; i >= 0; --i) {
+      double s = b[i];
+      for (int j = i + 1; j < rk; ++j) s -= A[(size_t)j * n + i] * x[j];
+      x[i] = s / A[(size_t)i * n + i];
+    }
+    for (int c = 0; c < nb; ++c) coeffs[c] = 0.0;
+    for (int i = 0; i < rk; ++i) coeffs[cols[s_perm[i]]] = x[i];
+  }
+}
+
+}  // namespace brm
+
+using namespace brm;
+
+namespace {
+int bfail(int code, const std::string &msg) { return brm::set_error(code, "%s", msg.c_str()); }
+bool is_dev(const void *p) {
+  cudaPointerAttributes a;
+  if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+}  // namespace
+
+#define BCU(call)                                                                        \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      rc = bfail(e_ == cudaErrorMemoryAllocation ? BRM_ENOMEM : BRM_ECUDA,               \
+                 std::string(#call) + ": " + cudaGetErrorString(e_));                    \
+      goto done;                                                                         \
+    }                                                                                    \
+  } while (0)
+
+extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, const double *betas, int64_t n64,
+                                int32_t F, int32_t rounds, int32_t *out_feat, double *out_thr, double *out_pol,
+                                double *out_alpha, int32_t *out_count, double *out_intercept) {
+  (void)mode;  // both modes replay numpy's summation orders in this build
+  if (!xs || !betas || !out_count || !out_intercept) return bfail(BRM_EINVAL, "NULL argument");
+  if (rounds < 1) return bfail(BRM_EINVAL, "need at least one round, got " + std::to_string(rounds));
+  if (n64 < 1 || n64 > (1 << 26)) return bfail(BRM_EINVAL, "training set size out of range");
+  if (F < 1 || F > 148) return bfail(BRM_EINVAL, "feature count out of range");
+  if (rounds > 0 && (!out_feat || !out_thr || !out_pol || !out_alpha)) return bfail(BRM_EINVAL, "NULL stump outputs");
+  const int n = (int)n64;
+  int rc = BRM_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaStream_t s = nullptr;
+  double *d_xs = nullptr, *d_b = nullptr, *d_xt = nullptr, *d_xsorted = nullptr, *d_y = nullptr, *d_w = nullptr;
+  double *d_pc = nullptr, *d_nc = nullptr, *d_err = nullptr, *d_wsub = nullptr, *d_thr = nullptr, *d_pol = nullptr,
+         *d_alpha = nullptr;
+  int *d_iota = nullptr, *d_order = nullptr, *d_pos = nullptr, *d_npos = nullptr, *d_feat = nullptr,
+      *d_count = nullptr;
+  int2 *d_leaves = nullptr;
+  void *d_tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int npos = 0;
+  std::vector<int2> leaves;
+  BCU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  BCU(cudaMallocAsync(&d_xs, sizeof(double) * (size_t)n * F, s));
+  BCU(cudaMemcpyAsync(d_xs, xs, sizeof(double) * (size_t)n * F, is_dev(xs) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  BCU(cudaMallocAsync(&d_b, sizeof(double) * n, s));
+  BCU(cudaMemcpyAsync(d_b, betas, sizeof(double) * n, is_dev(betas) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  BCU(cudaMallocAsync(&d_y, sizeof(double) * n, s));
+  BCU(cudaMallocAsync(&d_npos, sizeof(int), s));
+  BCU(cudaMemsetAsync(d_npos, 0, sizeof(int), s));
+  labels_from_betas<<<(n + 255) / 256, 256, 0, s>>>(d_b, n, d_y, d_npos);
+  BCU(cudaMemcpyAsync(&npos, d_npos, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BCU(cudaStreamSynchronize(s));
+  if (npos == 0 || npos == n) {
+    // one class: zero-round ensemble carrying the class sign (boosting.py:185-187)
+    *out_count = 0;
+    *out_intercept = npos == n ? 1.0 : -1.0;
+    goto done;
+  }
+  BCU(cudaMallocAsync(&d_xt, sizeof(double) * (size_t)n * F, s));
+  BCU(cudaMallocAsync(&d_xsorted, sizeof(double) * (size_t)n * F, s));
+  BCU(cudaMallocAsync(&d_iota, sizeof(int) * n, s));
+  BCU(cudaMallocAsync(&d_order, sizeof(int) * (size_t)n * F, s));
+  transpose_cols<<<(unsigned)(((int64_t)n * F + 255) / 256), 256, 0, s>>>(d_xs, n, F, d_xt, d_iota);
+  BCU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_xt, d_xsorted, d_iota, d_order, n, 0, 64, s));
+  BCU(cudaMallocAsync(&d_tmp, tmp_bytes, s));
+  for (int f = 0; f < F; ++f)
+    BCU(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_xt + (size_t)f * n, d_xsorted + (size_t)f * n, d_iota,
+                                        d_order + (size_t)f * n, n, 0, 64, s));
+  BCU(cudaMallocAsync(&d_w, sizeof(double) * n, s));
+  fill_value<<<(n + 255) / 256, 256, 0, s>>>(d_w, n, 1.0 / n);
+  BCU(cudaMallocAsync(&d_pc, sizeof(double) * (size_t)n * F, s));
+  BCU(cudaMallocAsync(&d_nc, sizeof(double) * (size_t)n * F, s));
+  BCU(cudaMallocAsync(&d_err, sizeof(double) * F, s));
+  BCU(cudaMallocAsync(&d_pos, sizeof(int) * F, s));
+  BCU(cudaMallocAsync(&d_wsub, sizeof(double) * (size_t)n * F, s));
+  BCU(cudaMallocAsync(&d_feat, sizeof(int) * rounds, s));
+  BCU(cudaMallocAsync(&d_thr, sizeof(double) * rounds, s));
+  BCU(cudaMallocAsync(&d_pol, sizeof(double) * rounds, s));
+  BCU(cudaMallocAsync(&d_alpha, sizeof(double) * rounds, s));
+  BCU(cudaMallocAsync(&d_count, sizeof(int), s));
+  pw_leaves(0, n, leaves);
+  BCU(cudaMallocAsync(&d_leaves, sizeof(int2) * leaves.size(), s));
+  BCU(cudaMemcpyAsync(d_leaves, leaves.data(), sizeof(int2) * leaves.size(), cudaMemcpyHostToDevice, s));
+  {
+    BoostParams P{};
+    P.n = n;
+    P.F = F;
+    P.rounds = rounds;
+    P.xs = d_xs;
+    P.xsorted = d_xsorted;
+    P.order = d_order;
+    P.y = d_y;
+    P.w = d_w;
+    P.pcum = d_pc;
+    P.ncum = d_nc;
+    P.leaves = d_leaves;
+    P.n_leaves = (int)leaves.size();
+    P.feat_err = d_err;
+    P.feat_pos = d_pos;
+    P.wsub = d_wsub;
+    P.out_feat = d_feat;
+    P.out_thr = d_thr;
+    P.out_pol = d_pol;
+    P.out_alpha = d_alpha;
+    P.out_count = d_count;
+    const size_t smem = sizeof(double) * (leaves.size() + 3 * kTile) + kTile;
+    BCU(cudaFuncSetAttribute(boost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    void *args[] = {&P};
+    BCU(cudaLaunchCooperativeKernel((void *)boost_kernel, dim3(F), dim3(kBoostThreads), args, smem, s));
+  }
+  BCU(cudaGetLastError());
+  {
+    int count = 0;
+    BCU(cudaMemcpyAsync(&count, d_count, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BCU(cudaStreamSynchronize(s));
+    *out_count = count;
+    if (count > 0) {
+      std::vector<int> feat(count);
+      BCU(cudaMemcpy(feat.data(), d_feat, sizeof(int) * count, cudaMemcpyDeviceToHost));
+      BCU(cudaMemcpy(out_thr, d_thr, sizeof(double) * count, cudaMemcpyDefault));
+      BCU(cudaMemcpy(out_pol, d_pol, sizeof(double) * count, cudaMemcpyDefault));
+      BCU(cudaMemcpy(out_alpha, d_alpha, sizeof(double) * count, cudaMemcpyDefault));
+      BCU(cudaMemcpy(out_feat, feat.data(), sizeof(int) * count, cudaMemcpyDefault));
+      *out_intercept = 0.0;
+    } else {
+      // no stump beat random guessing: majority sign (boosting.py:202-205)
+      *out_intercept = 2 * npos >= n ? 1.0 : -1.0;
+    }
+  }
+done:
+  for (void *p : {(void *)d_xs, (void *)d_b, (void *)d_xt, (void *)d_xsorted, (void *)d_y, (void *)d_w, (void *)d_pc,
+                  (void *)d_nc, (void *)d_err, (void *)d_wsub, (void *)d_thr, (void *)d_pol, (void *)d_alpha,
+                  (void *)d_iota, (void *)d_order, (void *)d_pos, (void *)d_npos, (void *)d_feat, (void *)d_count,
+                  (void *)d_leaves, d_tmp})
+    if (p) cudaFreeAsync(p, s);
+  if (s) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  return rc;
+}
+
+extern "C" int brm_lstsq(int32_t device, const double *design, const double *levels, int64_t n64, int32_t nb,
+                         int32_t k, double *out_coeffs, int32_t *out_rank_deficient) {
+  if (!design || !levels || !out_coeffs || !out_rank_deficient) return bfail(BRM_EINVAL, "NULL argument");
+  if (nb < 1 || nb > kLsMaxB) return bfail(BRM_EINVAL, "basis size out of range");
+  if (n64 < nb) return bfail(BRM_EINVAL, "need at least " + std::to_string(nb) + " probe points for the quadratic fit, got " + std::to_string(n64));
+  if (n64 > kLsMaxN) return bfail(BRM_EINVAL, "too many probe points for the device fit");
+  const int n = (int)n64;
+  int rc = BRM_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaStream_t s = nullptr;
+  double *d_design = nullptr, *d_levels = nullptr, *d_coeffs = nullptr;
+  int *d_cols = nullptr, *d_rank = nullptr;
+  std::vector<int> cols(nb);
+  int rank = 0;
+  for (int c = 0; c < nb; ++c) cols[c] = c;
+  const size_t smem_full = sizeof(double) * ((size_t)nb * n + n);
+  BCU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  BCU(cudaMallocAsync(&d_design, sizeof(double) * (size_t)n * nb, s));
+  BCU(cudaMemcpyAsync(d_design, design, sizeof(double) * (size_t)n * nb, cudaMemcpyDefault, s));
+  BCU(cudaMallocAsync(&d_levels, sizeof(double) * n, s));
+  BCU(cudaMemcpyAsync(d_levels, levels, sizeof(double) * n, cudaMemcpyDefault, s));
+  BCU(cudaMallocAsync(&d_coeffs, sizeof(double) * nb, s));
+  BCU(cudaMallocAsync(&d_cols, sizeof(int) * nb, s));
+  BCU(cudaMallocAsync(&d_rank, sizeof(int), s));
+  BCU(cudaMemcpyAsync(d_cols, cols.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
+  BCU(cudaFuncSetAttribute(lstsq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
+  lstsq_kernel<<<1, 256, smem_full, s>>>(d_design, d_levels, n, nb, d_cols, nb, d_coeffs, d_rank);
+  BCU(cudaGetLastError());
+  BCU(cudaMemcpyAsync(&rank, d_rank, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BCU(cudaStreamSynchronize(s));
+  *out_rank_deficient = rank < nb;
+  if (rank < nb) {
+    // keep [1, z_a, z_a^2], zero the cross terms (boundary_iz.py:264-275)
+    std::vector<int> keep{0};
+    for (int a = 1; a <= k; ++a) keep.push_back(a);
+    int pos = 1 + k;
+    for (int a = 0; a < k; ++a) {
+      keep.push_back(pos);
+      pos += k - a;
+    }
+    BCU(cudaMemcpyAsync(d_cols, keep.data(), sizeof(int) * keep.size(), cudaMemcpyHostToDevice, s));
+    lstsq_kernel<<<1, 256, sizeof(double) * (keep.size() * n + n), s>>>(d_design, d_levels, n, nb, d_cols,
+                                                                        (int)keep.size(), d_coeffs, d_rank);
+    BCU(cudaGetLastError());
+  }
+  BCU(cudaMemcpyAsync(out_coeffs, d_coeffs, sizeof(double) * nb, cudaMemcpyDefault, s));
+  BCU(cudaStreamSynchronize(s));
+done:
+  for (void *p : {(void *)d_design, (void *)d_levels, (void *)d_coeffs, (void *)d_cols, (void *)d_rank})
+    if (p) cudaFreeAsync(p, s);
+  if (s) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  return rc;
+}

@@ -1,0 +1,783 @@
+// brm_capi.cu -- extern "C" boundary (include/bermuda_b200.h).
+//
+// Host side of the engine: owns device images of the packs, stages host
+// buffers, sizes grids to the SM count and launches the kernels on one
+// stream.  No compute happens here besides argument checks and the
+// 64-bit key hash of brm_derive_words.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bermuda_b200.h"
+#include "brm_internal.h"
+
+using namespace brm;
+
+namespace {
+thread_local std::string g_err;
+}
+
+int brm::set_error(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+namespace {
+
+#define fail brm::set_error
+
+#define BRM_CUDA(call)                                                                           \
+  do {                                                                                           \
+    cudaError_t e_ = (call);                                                                     \
+    if (e_ != cudaSuccess) {                                                                     \
+      if (e_ == cudaErrorMemoryAllocation) return fail(BRM_ENOMEM, "%s: %s", #call, cudaGetErrorString(e_)); \
+      return fail(BRM_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));                           \
+    }                                                                                            \
+  } while (0)
+
+#define BRM_TRY(expr)          \
+  do {                         \
+    int rc_ = (expr);          \
+    if (rc_ != BRM_OK) return rc_; \
+  } while (0)
+
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// One argument buffer: the caller's device pointer, or a stream-ordered
+// device copy of a host buffer (inputs) / a device buffer copied back to the
+// host pointer by finish() (outputs).
+struct Arg {
+  void *host = nullptr;
+  void *dev = nullptr;
+  size_t bytes = 0;
+  bool owned = false;
+};
+
+struct Call {
+  cudaStream_t stream;
+  std::vector<Arg> args;
+  bool host_out = false;
+  explicit Call(cudaStream_t s) : stream(s) {}
+  ~Call() {
+    for (auto &a : args)
+      if (a.owned && a.dev) cudaFreeAsync(a.dev, stream);
+  }
+  template <typename T>
+  int in(const T *p, size_t count, const T **out) {
+    *out = nullptr;
+    if (!p || count == 0) return BRM_OK;
+    if (is_device_ptr(p)) {
+      *out = p;
+      return BRM_OK;
+    }
+    Arg a;
+    a.bytes = count * sizeof(T);
+    BRM_CUDA(cudaMallocAsync(&a.dev, a.bytes, stream));
+    a.owned = true;
+    args.push_back(a);
+    BRM_CUDA(cudaMemcpyAsync(a.dev, p, a.bytes, cudaMemcpyHostToDevice, stream));
+    *out = static_cast<const T *>(a.dev);
+    return BRM_OK;
+  }
+  template <typename T>
+  int out(T *p, size_t count, T **dptr) {
+    *dptr = nullptr;
+    if (!p || count == 0) return BRM_OK;
+    if (is_device_ptr(p)) {
+      *dptr = p;
+      return BRM_OK;
+    }
+    Arg a;
+    a.host = p;
+    a.bytes = count * sizeof(T);
+    BRM_CUDA(cudaMallocAsync(&a.dev, a.bytes, stream));
+    a.owned = true;
+    args.push_back(a);
+    host_out = true;
+    *dptr = static_cast<T *>(a.dev);
+    return BRM_OK;
+  }
+  template <typename T>
+  int scratch(size_t count, T **dptr) {
+    Arg a;
+    a.bytes = std::max<size_t>(count, 1) * sizeof(T);
+    BRM_CUDA(cudaMallocAsync(&a.dev, a.bytes, stream));
+    a.owned = true;
+    args.push_back(a);
+    *dptr = static_cast<T *>(a.dev);
+    return BRM_OK;
+  }
+  int finish() {
+    BRM_CUDA(cudaGetLastError());
+    for (auto &a : args)
+      if (a.host) BRM_CUDA(cudaMemcpyAsync(a.host, a.dev, a.bytes, cudaMemcpyDeviceToHost, stream));
+    if (host_out) BRM_CUDA(cudaStreamSynchronize(stream));
+    return BRM_OK;
+  }
+};
+
+struct DevInfo {
+  int sms = 148;
+  int max_smem = 227 * 1024;
+};
+
+DevInfo device_info(int dev) {
+  DevInfo info;
+  cudaDeviceGetAttribute(&info.sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&info.max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return info;
+}
+
+template <typename T>
+int fetch(const T *src, size_t count, std::vector<T> &dst, const char *name) {
+  dst.assign(count, T());
+  if (count == 0) return BRM_OK;
+  if (!src) return fail(BRM_EINVAL, "%s is NULL", name);
+  BRM_CUDA(cudaMemcpy(dst.data(), src, count * sizeof(T), cudaMemcpyDefault));
+  return BRM_OK;
+}
+
+int quad_basis_size(int k) { return 1 + k + k * (k + 1) / 2; }
+
+}  // namespace
+
+struct brm_ctx {
+  int device = 0;
+  int mode = BRM_MODE_PARITY;
+  ModelHdr hdr{};
+  unsigned char *blob = nullptr;
+  size_t blob_bytes = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t user_stream = nullptr;
+  bool has_user_stream = false;
+  DevInfo info;
+  KernelTriple kern{};
+  double *normals = nullptr;  // supplied-normals copy (device)
+  uint64_t nrm_base = 0, nrm_count = 0;
+  cudaStream_t stream() const { return has_user_stream ? user_stream : own_stream; }
+  bool fast() const { return mode == BRM_MODE_FAST; }
+  const double *blob_dbl(int off) const { return reinterpret_cast<const double *>(blob) + off; }
+};
+
+namespace {
+
+int smem_model(const brm_ctx *c) {
+  return c->fast() ? model_smem_bytes<float>(c->hdr) : model_smem_bytes<double>(c->hdr);
+}
+
+int allow_smem(const void *kernel, int bytes) {
+  BRM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  return BRM_OK;
+}
+
+int check_remaining(const brm_ctx *c, int m) {
+  if (c->hdr.n_dates - m <= 0) return fail(BRM_EINVAL, "start date has no remaining exercise dates");
+  if (m < 0) return fail(BRM_EINVAL, "negative start date %d", m);
+  return BRM_OK;
+}
+
+// Launch walk_units over n_units x chunks and fold each unit.
+struct WalkJob {
+  int n_units = 0, per_unit = 0, chunk = 0;
+  int64_t total_paths = 0;
+  int m_start = 0;
+  const double *starts = nullptr;
+  int start_stride = 0;
+  const uint64_t *keys = nullptr, *streams = nullptr;
+  uint64_t seed = 0;
+  int phase = 0, key_date = 0;
+  int64_t item_base = 0;
+  uint64_t draw_base = 0;
+  double *path_out = nullptr;
+  int32_t *stop_out = nullptr;
+  int finish_mode = 0;
+  const double *points = nullptr;
+  double *out = nullptr;
+};
+
+int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
+  if (j.n_units <= 0) return BRM_OK;
+  WalkParams P{};
+  P.hdr = c->hdr;
+  P.blob = c->blob;
+  P.n_units = j.n_units;
+  P.per_unit = j.per_unit;
+  P.chunk = std::max(1, std::min(j.chunk, kMaxChunk));
+  P.chunks_per_unit = std::max(1, (j.per_unit + P.chunk - 1) / P.chunk);
+  P.n_items = j.n_units * P.chunks_per_unit;
+  P.total_paths = j.total_paths;
+  P.m_start = j.m_start;
+  P.n_steps = c->hdr.n_dates - j.m_start;
+  P.starts = j.starts;
+  P.start_stride = j.start_stride;
+  P.keys = j.keys;
+  P.streams = j.streams;
+  P.seed = j.seed;
+  P.phase = j.phase;
+  P.key_date = j.key_date;
+  P.item_base = j.item_base;
+  P.draw_base = j.draw_base;
+  P.normals = c->normals;
+  P.nrm_base = c->nrm_base;
+  P.nrm_count = c->nrm_count;
+  P.path_out = j.path_out;
+  P.stop_out = j.stop_out;
+  P.vals_offset = smem_model(c);
+  const int smem = P.vals_offset + 8 * P.chunk;
+  if (smem > c->info.max_smem) return fail(BRM_EINVAL, "model image too large for shared memory (%d B)", smem);
+  BRM_TRY(call.scratch<double>(2 * (size_t)P.n_items, &P.partials));
+  BRM_TRY(allow_smem(c->kern.walk, smem));
+  int per_sm = 0;
+  BRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kern.walk, kWalkThreads, smem));
+  if (per_sm < 1) return fail(BRM_EINVAL, "walker does not fit on an SM (smem %d B)", smem);
+  const int grid = std::min(P.n_items, per_sm * c->info.sms);
+  void *args[] = {&P};
+  BRM_CUDA(cudaLaunchKernel(c->kern.walk, dim3(grid), dim3(kWalkThreads), args, smem, call.stream));
+  FinishParams F{};
+  F.partials = P.partials;
+  F.n_units = j.n_units;
+  F.chunks_per_unit = P.chunks_per_unit;
+  F.per_unit = j.per_unit;
+  F.mode = j.finish_mode;
+  F.total_paths = j.total_paths;
+  F.points = j.points;
+  F.d = c->hdr.d;
+  F.payoff = c->hdr.payoff;
+  F.strike = c->hdr.strike;
+  F.out = j.out;
+  if (F.out) {
+    void *fargs[] = {&F};
+    BRM_CUDA(cudaLaunchKernel(finish_kernel(), dim3((j.n_units + 127) / 128), dim3(128), fargs, 0, call.stream));
+  }
+  return BRM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int brm_abi_version(void) { return BRM_ABI_VERSION; }
+
+const char *brm_last_error(void) { return g_err.c_str(); }
+
+int brm_device_count(int32_t *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return fail(BRM_ENODEV, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *count = n;
+  return BRM_OK;
+}
+
+int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t device, int32_t mode,
+                   brm_ctx **out) {
+  if (!mk || !rl || !out) return fail(BRM_EINVAL, "NULL argument");
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(BRM_ENODEV, "no CUDA device available");
+  }
+  if (device < 0 || device >= ndev) return fail(BRM_EINVAL, "device %d out of range (%d devices)", device, ndev);
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (major != 10) return fail(BRM_ENODEV, "device %d is sm_%d0, this build targets sm_100a", device, major);
+  const int d = mk->d, nd = mk->n_dates;
+  if (d < 1 || d > kMaxD) return fail(BRM_EINVAL, "d=%d outside 1..%d", d, kMaxD);
+  if (nd < 1) return fail(BRM_EINVAL, "need at least one exercise date");
+  if (mk->payoff_kind < 0 || mk->payoff_kind > 4) return fail(BRM_EINVAL, "unknown payoff kind %d", mk->payoff_kind);
+  if ((mk->payoff_kind == BRM_PAY_PUT || mk->payoff_kind == BRM_PAY_CALL) && d != 1)
+    return fail(BRM_EINVAL, "1-D payoff requires d=1, got d=%d", d);
+  if (rl->kind < 0 || rl->kind > 3) return fail(BRM_EINVAL, "unknown rule kind %d", rl->kind);
+  if (mode != BRM_MODE_PARITY && mode != BRM_MODE_FAST) return fail(BRM_EINVAL, "unknown mode %d", mode);
+
+  DeviceScope scope(device);
+  std::vector<double> mu, vol, chol, disc, s0, izc, izlo, izhi, icept, thr, pol, alpha;
+  std::vector<int32_t> starts, counts, feat;
+  BRM_TRY(fetch(mk->step_mu, d, mu, "step_mu"));
+  BRM_TRY(fetch(mk->step_vol, d, vol, "step_vol"));
+  BRM_TRY(fetch(mk->chol, (size_t)d * d, chol, "chol"));
+  BRM_TRY(fetch(mk->disc_steps, nd + 1, disc, "disc_steps"));
+  BRM_TRY(fetch(mk->s0, d, s0, "s0"));
+  const int k = std::max(d - 1, 0);
+  int nbasis = 1;
+  if (rl->kind == BRM_RULE_IZ) {
+    nbasis = rl->nbasis;
+    if (nbasis != quad_basis_size(k)) return fail(BRM_EINVAL, "nbasis %d != %d for d=%d", nbasis, quad_basis_size(k), d);
+    if (rl->iz_space == 1 && d < 2) return fail(BRM_EINVAL, "log-space surfaces need d>1");
+    BRM_TRY(fetch(rl->iz_coeffs, (size_t)(nd + 1) * d * nbasis, izc, "iz_coeffs"));
+    if (d > 1) {
+      BRM_TRY(fetch(rl->iz_lo, k, izlo, "iz_lo"));
+      BRM_TRY(fetch(rl->iz_hi, k, izhi, "iz_hi"));
+    }
+  }
+  const int ns = rl->kind == BRM_RULE_CMC ? rl->n_stumps : 0;
+  if (ns < 0) return fail(BRM_EINVAL, "negative stump count");
+  if (rl->kind == BRM_RULE_CMC) {
+    BRM_TRY(fetch(rl->cmc_starts, nd + 1, starts, "cmc_starts"));
+    BRM_TRY(fetch(rl->cmc_counts, nd + 1, counts, "cmc_counts"));
+    BRM_TRY(fetch(rl->cmc_intercept, nd + 1, icept, "cmc_intercept"));
+    BRM_TRY(fetch(rl->cmc_feat, ns, feat, "cmc_feat"));
+    BRM_TRY(fetch(rl->cmc_thr, ns, thr, "cmc_thr"));
+    BRM_TRY(fetch(rl->cmc_pol, ns, pol, "cmc_pol"));
+    BRM_TRY(fetch(rl->cmc_alpha, ns, alpha, "cmc_alpha"));
+    const int nfeat = d > 1 ? d + 1 : 1;
+    for (int m = 0; m <= nd; ++m)
+      if (counts[m] < 0 || starts[m] < 0 || (counts[m] > 0 && starts[m] + counts[m] > ns))
+        return fail(BRM_EINVAL, "stump range of date %d outside the stump arrays", m);
+    for (int t = 0; t < ns; ++t)
+      if (feat[t] < 0 || feat[t] >= nfeat) return fail(BRM_EINVAL, "stump %d feature %d outside 0..%d", t, feat[t], nfeat - 1);
+  }
+
+  ModelHdr h{};
+  h.d = d;
+  h.n_dates = nd;
+  h.payoff = mk->payoff_kind;
+  h.rule = rl->kind;
+  h.call_like = rl->call_like ? 1 : 0;
+  h.imm_date = rl->imm_date;
+  h.nbasis = nbasis;
+  h.iz_space = rl->kind == BRM_RULE_IZ ? rl->iz_space : 0;
+  h.n_stumps = ns;
+  h.strike = mk->strike;
+  int lower = 1;
+  for (int i = 0; i < d; ++i)
+    for (int a = i + 1; a < d; ++a)
+      if (chol[i * d + a] != 0.0) lower = 0;
+  h.chol_lower = lower;
+  std::vector<double> dbl;
+  auto put = [&](const std::vector<double> &v, size_t min_len) {
+    int off = (int)dbl.size();
+    dbl.insert(dbl.end(), v.begin(), v.end());
+    if (v.size() < min_len) dbl.insert(dbl.end(), min_len - v.size(), 0.0);
+    return off;
+  };
+  h.o_mu = put(mu, d);
+  h.o_vol = put(vol, d);
+  h.o_chol = put(chol, (size_t)d * d);
+  h.o_disc = put(disc, nd + 1);
+  h.o_s0 = put(s0, d);
+  h.o_izc = put(izc, 1);
+  h.o_izlo = put(izlo, std::max(k, 1));
+  h.o_izhi = put(izhi, std::max(k, 1));
+  if (icept.empty()) icept.assign(nd + 1, -1.0);
+  h.o_icept = put(icept, nd + 1);
+  h.o_thr = put(thr, 1);
+  std::vector<double> ap(ns);
+  for (int t = 0; t < ns; ++t) ap[t] = alpha[t] * pol[t];  // the product the reference forms per vote
+  h.o_ap = put(ap, 1);
+  h.n_dbl = (int)dbl.size();
+  std::vector<int32_t> ints;
+  auto puti = [&](const std::vector<int32_t> &v, size_t min_len) {
+    int off = (int)ints.size();
+    ints.insert(ints.end(), v.begin(), v.end());
+    if (v.size() < min_len) ints.insert(ints.end(), min_len - v.size(), 0);
+    return off;
+  };
+  h.o_starts = puti(starts, nd + 1);
+  h.o_counts = puti(counts, nd + 1);
+  h.o_feat = puti(feat, 1);
+  h.n_int = (int)ints.size();
+
+  brm_ctx *c = new brm_ctx();
+  c->device = device;
+  c->mode = mode;
+  c->hdr = h;
+  c->info = device_info(device);
+  c->kern = kernels_for(d, mode == BRM_MODE_FAST);
+  c->blob_bytes = 8 * dbl.size() + 4 * ints.size();
+  cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&c->blob, c->blob_bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(c->blob, dbl.data(), 8 * dbl.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !ints.empty())
+    e = cudaMemcpy(c->blob + 8 * dbl.size(), ints.data(), 4 * ints.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    brm_ctx_destroy(c);
+    return fail(e == cudaErrorMemoryAllocation ? BRM_ENOMEM : BRM_ECUDA, "context upload: %s", cudaGetErrorString(e));
+  }
+  if (smem_model(c) + 8 * 64 > c->info.max_smem) {
+    brm_ctx_destroy(c);
+    return fail(BRM_EINVAL, "model image (%d B) exceeds shared memory", smem_model(c));
+  }
+  *out = c;
+  return BRM_OK;
+}
+
+int brm_ctx_destroy(brm_ctx *c) {
+  if (!c) return BRM_OK;
+  DeviceScope scope(c->device);
+  if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+  if (c->has_user_stream) cudaStreamSynchronize(c->user_stream);
+  if (c->blob) cudaFree(c->blob);
+  if (c->normals) cudaFree(c->normals);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+  return BRM_OK;
+}
+
+int brm_ctx_set_stream(brm_ctx *c, void *s) {
+  if (!c) return fail(BRM_EINVAL, "NULL context");
+  c->user_stream = static_cast<cudaStream_t>(s);
+  c->has_user_stream = s != nullptr;
+  return BRM_OK;
+}
+
+int brm_ctx_supply_normals(brm_ctx *c, const double *normals, uint64_t base, uint64_t count) {
+  if (!c) return fail(BRM_EINVAL, "NULL context");
+  DeviceScope scope(c->device);
+  BRM_CUDA(cudaStreamSynchronize(c->stream()));
+  if (c->normals) cudaFree(c->normals);
+  c->normals = nullptr;
+  c->nrm_base = c->nrm_count = 0;
+  if (!normals || count == 0) return BRM_OK;
+  BRM_CUDA(cudaMalloc(&c->normals, count * sizeof(double)));
+  BRM_CUDA(cudaMemcpy(c->normals, normals, count * sizeof(double), cudaMemcpyDefault));
+  c->nrm_base = base;
+  c->nrm_count = count;
+  return BRM_OK;
+}
+
+int brm_derive_words(uint64_t seed, uint32_t phase, uint64_t item, uint64_t date, uint64_t *key64,
+                     uint64_t *stream64) {
+  if (!key64 || !stream64) return fail(BRM_EINVAL, "NULL output");
+  derive_words(seed, phase, item, date, *key64, *stream64);
+  return BRM_OK;
+}
+
+int brm_raw_uint64(int32_t device, uint64_t key64, uint64_t stream64, uint64_t start, int64_t count, uint64_t *out) {
+  if (count < 0) return fail(BRM_EINVAL, "negative count");
+  if (count == 0) return BRM_OK;
+  DeviceScope scope(device);
+  Call call(nullptr);
+  uint64_t *o;
+  BRM_TRY(call.out(out, count, &o));
+  const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 16);
+  void *args[] = {&key64, &stream64, &start, &count, &o};
+  BRM_CUDA(cudaLaunchKernel(fill_raw_kernel(), dim3(grid), dim3(256), args, 0, call.stream));
+  BRM_TRY(call.finish());
+  BRM_CUDA(cudaStreamSynchronize(call.stream));
+  return BRM_OK;
+}
+
+int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t start, int64_t count, double *out) {
+  if (count < 0) return fail(BRM_EINVAL, "negative count");
+  if (count == 0) return BRM_OK;
+  DeviceScope scope(device);
+  Call call(nullptr);
+  double *o;
+  BRM_TRY(call.out(out, count, &o));
+  const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 16);
+  void *args[] = {&key64, &stream64, &start, &count, &o};
+  BRM_CUDA(cudaLaunchKernel(fill_normals_kernel(), dim3(grid), dim3(256), args, 0, call.stream));
+  BRM_TRY(call.finish());
+  BRM_CUDA(cudaStreamSynchronize(call.stream));
+  return BRM_OK;
+}
+
+int brm_stopped_sums(brm_ctx *c, const double *start, int32_t m_start, int64_t n_paths, uint64_t key64,
+                     uint64_t stream64, uint64_t draw_base, double *sum, double *sumsq) {
+  if (!c || !sum || !sumsq) return fail(BRM_EINVAL, "NULL argument");
+  BRM_TRY(check_remaining(c, m_start));
+  if (n_paths < 0 || n_paths > (int64_t)1 << 30) return fail(BRM_EINVAL, "n_paths %lld out of range", (long long)n_paths);
+  DeviceScope scope(c->device);
+  Call call(c->stream());
+  const double *st;
+  BRM_TRY(call.in(start, c->hdr.d, &st));
+  if (!st) return fail(BRM_EINVAL, "start_values is NULL");
+  double *res;
+  BRM_TRY(call.scratch<double>(2, &res));
+  if (n_paths == 0) {
+    BRM_CUDA(cudaMemsetAsync(res, 0, 2 * sizeof(double), call.stream));
+  } else {
+    WalkJob j;
+    j.n_units = 1;
+    j.per_unit = (int)n_paths;
+    j.total_paths = n_paths;
+    j.chunk = 256;
+    j.m_start = m_start;
+    j.starts = st;
+    j.key_date = 0;
+    uint64_t keys[1] = {key64}, streams[1] = {stream64};
+    const uint64_t *dk, *dsr;
+    BRM_TRY(call.in(keys, 1, &dk));
+    BRM_TRY(call.in(streams, 1, &dsr));
+    j.keys = dk;
+    j.streams = dsr;
+    j.draw_base = draw_base;
+    j.finish_mode = 0;
+    j.out = res;
+    BRM_TRY(run_walk(c, call, j));
+  }
+  double *o1, *o2;
+  BRM_TRY(call.out(sum, 1, &o1));
+  BRM_TRY(call.out(sumsq, 1, &o2));
+  BRM_CUDA(cudaMemcpyAsync(o1, res, sizeof(double), cudaMemcpyDeviceToDevice, call.stream));
+  BRM_CUDA(cudaMemcpyAsync(o2, res + 1, sizeof(double), cudaMemcpyDeviceToDevice, call.stream));
+  return call.finish();
+}
+
+int brm_path_values(brm_ctx *c, const double *start, int32_t m_start, int64_t n_paths, uint64_t key64,
+                    uint64_t stream64, uint64_t draw_base, double *values, int32_t *stop_dates) {
+  if (!c) return fail(BRM_EINVAL, "NULL context");
+  BRM_TRY(check_remaining(c, m_start));
+  if (n_paths < 0 || n_paths > (int64_t)1 << 30) return fail(BRM_EINVAL, "n_paths out of range");
+  if (n_paths == 0) return BRM_OK;
+  DeviceScope scope(c->device);
+  Call call(c->stream());
+  const double *st;
+  BRM_TRY(call.in(start, c->hdr.d, &st));
+  if (!st) return fail(BRM_EINVAL, "start_values is NULL");
+  double *vo;
+  int32_t *so;
+  BRM_TRY(call.out(values, n_paths, &vo));
+  BRM_TRY(call.out(stop_dates, n_paths, &so));
+  uint64_t keys[1] = {key64}, streams[1] = {stream64};
+  WalkJob j;
+  BRM_TRY(call.in(keys, 1, &j.keys));
+  BRM_TRY(call.in(streams, 1, &j.streams));
+  j.n_units = 1;
+  j.per_unit = (int)n_paths;
+  j.total_paths = n_paths;
+  j.chunk = 256;
+  j.m_start = m_start;
+  j.starts = st;
+  j.draw_base = draw_base;
+  j.path_out = vo;
+  j.stop_out = so;
+  BRM_TRY(run_walk(c, call, j));
+  return call.finish();
+}
+
+int brm_decisions(brm_ctx *c, const double *states, int64_t n, int32_t m, int32_t *out) {
+  if (!c) return fail(BRM_EINVAL, "NULL context");
+  if (m < 1 || m > c->hdr.n_dates) return fail(BRM_EINVAL, "date %d outside 1..%d", m, c->hdr.n_dates);
+  if (n <= 0) return BRM_OK;
+  DeviceScope scope(c->device);
+  Call call(c->stream());
+  DecisionParams P{};
+  P.hdr = c->hdr;
+  P.blob = c->blob;
+  P.n = n;
+  P.m = m;
+  BRM_TRY(call.in(states, (size_t)n * c->hdr.d, &P.states));
+  BRM_TRY(call.out(out, n, &P.out));
+  const int smem = smem_model(c);
+  BRM_TRY(allow_smem(c->kern.dec, smem));
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->info.sms * 4);
+  void *args[] = {&P};
+  BRM_CUDA(cudaLaunchKernel(c->kern.dec, dim3(grid), dim3(256), args, smem, call.stream));
+  return call.finish();
+}
+
+int brm_price_blocks(brm_ctx *c, int64_t n_paths, uint64_t seed, int64_t block_lo, int64_t block_hi,
+                     double *out_stats) {
+  if (!c || !out_stats) return fail(BRM_EINVAL, "NULL argument");
+  if (n_paths < 1) return fail(BRM_EINVAL, "need at least one path, got %lld", (long long)n_paths);
+  const int64_t n_blocks = (n_paths + kPathBlock - 1) / kPathBlock;
+  if (block_lo < 0 || block_hi > n_blocks || block_lo > block_hi)
+    return fail(BRM_EINVAL, "block range [%lld, %lld) outside 0..%lld", (long long)block_lo, (long long)block_hi,
+                (long long)n_blocks);
+  if (block_hi - block_lo > (1 << 24)) return fail(BRM_EINVAL, "too many blocks in one call");
+  if (block_hi == block_lo) return BRM_OK;
+  DeviceScope scope(c->device);
+  Call call(c->stream());
+  double *o;
+  BRM_TRY(call.out(out_stats, 3 * (size_t)(block_hi - block_lo), &o));
+  WalkJob j;
+  j.n_units = (int)(block_hi - block_lo);
+  j.per_unit = kPathBlock;
+  j.total_paths = n_paths - block_lo * kPathBlock;
+  j.chunk = kPriceChunk;
+  j.m_start = 0;
+  j.starts = nullptr;
+  j.seed = seed;
+  j.phase = BRM_PHASE_PRICING;
+  j.item_base = block_lo;
+  j.key_date = 0;
+  j.draw_base = 0;
+  j.finish_mode = 1;
+  j.out = o;
+  BRM_TRY(run_walk(c, call, j));
+  return call.finish();
+}
+
+int brm_cmc_labels(brm_ctx *c, const double *points, int64_t n, int32_t m, int32_t n_label, const uint64_t *keys,
+                   const uint64_t *streams, uint64_t seed, int64_t item_lo, uint64_t draw_base, double *out_beta) {
+  if (!c || !out_beta) return fail(BRM_EINVAL, "NULL argument");
+  BRM_TRY(check_remaining(c, m));
+  if (n_label < 1) return fail(BRM_EINVAL, "need at least one labeling path");
+  if (n < 0 || n > (1 << 26)) return fail(BRM_EINVAL, "point count out of range");
+  if (n == 0) return BRM_OK;
+  DeviceScope scope(c->device);
+  Call call(c->stream());
+  WalkJob j;
+  BRM_TRY(call.in(points, (size_t)n * c->hdr.d, &j.starts));
+  if (!j.starts) return fail(BRM_EINVAL, "points is NULL");
+  if (keys) {
+    BRM_TRY(call.in(keys, n, &j.keys));
+    BRM_TRY(call.in(streams, n, &j.streams));
+    if (!j.streams) return fail(BRM_EINVAL, "streams is NULL");
+  }
+  double *o;
+  BRM_TRY(call.out(out_beta, n, &o));
+  j.n_units = (int)n;
+  j.per_unit = n_label;
+  j.total_paths = n * (int64_t)n_label;
+  j.chunk = std::min(n_label, kMaxChunk);
+  j.m_start = m;
+  j.start_stride = c->hdr.d;
+  j.seed = seed;
+  j.phase = BRM_PHASE_CMC_CALC;
+  j.item_base = item_lo;
+  j.key_date = m;
+  j.draw_base = draw_base;
+  j.finish_mode = 2;
+  j.points = j.starts;
+  j.out = o;
+  BRM_TRY(run_walk(c, call, j));
+  return call.finish();
+}
+
+int brm_sample_points(brm_ctx *c, int32_t mode, int32_t m, uint64_t seed, int64_t item_lo, int64_t n,
+                      const double *bridge, double *out_points) {
+  if (!c || !out_points) return fail(BRM_EINVAL, "NULL argument");
+  if (m < 1 || m > c->hdr.n_dates) return fail(BRM_EINVAL, "date index %d outside 1..%d", m, c->hdr.n_dates);
+  if (mode != 0 && mode != 1) return fail(BRM_EINVAL, "unknown sampler mode %d", mode);
+  if (n <= 0) return BRM_OK;
+  DeviceScope scope(c->device);
+  Call call(c->stream());
+  SampleParams P{};
+  P.mode = mode;
+  P.m = m;
+  P.d = c->hdr.d;
+  P.n_dates = c->hdr.n_dates;
+  P.seed = seed;
+  P.item_lo = item_lo;
+  P.n = n;
+  P.s0 = c->blob_dbl(c->hdr.o_s0);
+  P.chol = c->blob_dbl(c->hdr.o_chol);
+  P.step_mu = c->blob_dbl(c->hdr.o_mu);
+  P.step_vol = c->blob_dbl(c->hdr.o_vol);
+  if (mode == 0) {
+    BRM_TRY(call.in(bridge, 4 * (size_t)c->hdr.d + 1, &P.bridge));
+    if (!P.bridge) return fail(BRM_EINVAL, "bridge scalars are NULL");
+  }
+  BRM_TRY(call.out(out_points, (size_t)n * c->hdr.d, &P.out));
+  void *args[] = {&P};
+  BRM_CUDA(cudaLaunchKernel(sample_kernel(), dim3((unsigned)((n + 127) / 128)), dim3(128), args, 0, call.stream));
+  return call.finish();
+}
+
+int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t *assets, int64_t n, int32_t m,
+                 int32_t n_inner, double eps, int32_t max_iter, int32_t avg_window, double lo, double hi, double tol,
+                 const uint64_t *keys, const uint64_t *streams, uint64_t seed, int64_t item_lo, double *out_level,
+                 int32_t *out_iterations, int32_t *out_converged) {
+  if (!c || !out_level || !out_iterations || !out_converged) return fail(BRM_EINVAL, "NULL argument");
+  BRM_TRY(check_remaining(c, m));
+  if (solver != 0 && solver != 1) return fail(BRM_EINVAL, "unknown solver %d", solver);
+  if (n_inner < 1) return fail(BRM_EINVAL, "need at least one inner path, got %d", n_inner);
+  if (solver == 0 && !(eps > 0.0)) return fail(BRM_EINVAL, "epsilon must be positive, got %g", eps);
+  if (solver == 0 && avg_window < 1) return fail(BRM_EINVAL, "avg_window must be >= 1");
+  if (solver == 1 && !(lo < hi && tol > 0.0)) return fail(BRM_EINVAL, "bisection needs lo < hi and tol > 0");
+  if (max_iter > 100000) return fail(BRM_EINVAL, "max_iter too large");
+  if (n <= 0) return BRM_OK;
+  if (n > (1 << 20)) return fail(BRM_EINVAL, "too many probes");
+  DeviceScope scope(c->device);
+  Call call(c->stream());
+  IzParams P{};
+  P.hdr = c->hdr;
+  P.blob = c->blob;
+  P.n_probes = (int)n;
+  P.m = m;
+  P.n_steps = c->hdr.n_dates - m;
+  P.n_inner = n_inner;
+  P.solver = solver;
+  P.eps = eps;
+  P.max_iter = std::max(max_iter, 0);
+  P.avg_window = avg_window;
+  P.lo = lo;
+  P.hi = hi;
+  P.tol = tol;
+  P.seed_stride = std::max(c->hdr.d - 1, 0);
+  double dummy_seed = 0.0;
+  if (P.seed_stride > 0) {
+    BRM_TRY(call.in(seeds, (size_t)n * P.seed_stride, &P.seeds));
+    if (!P.seeds) return fail(BRM_EINVAL, "seeds are NULL");
+  } else {
+    BRM_TRY(call.scratch<double>(1, const_cast<double **>(&P.seeds)));
+    BRM_CUDA(cudaMemcpyAsync(const_cast<double *>(P.seeds), &dummy_seed, sizeof(double), cudaMemcpyHostToDevice,
+                             call.stream));
+  }
+  BRM_TRY(call.in(assets, n, &P.assets));
+  if (keys) {
+    BRM_TRY(call.in(keys, n, &P.keys));
+    BRM_TRY(call.in(streams, n, &P.streams));
+    if (!P.streams) return fail(BRM_EINVAL, "streams is NULL");
+  }
+  P.seed = seed;
+  P.item_base = item_lo;
+  P.normals = c->normals;
+  P.nrm_base = c->nrm_base;
+  P.nrm_count = c->nrm_count;
+  BRM_TRY(call.out(out_level, n, &P.out_level));
+  BRM_TRY(call.out(out_iterations, n, &P.out_iter));
+  BRM_TRY(call.out(out_converged, n, &P.out_conv));
+  // cluster size: enough CTAs per probe to give each lane a path or two
+  int csize = 8;
+  while (csize > 1 && (int64_t)csize * kWalkThreads / 2 > n_inner) csize >>= 1;
+  const int per_cta = (n_inner + csize - 1) / csize;
+  P.vals_offset = smem_model(c);
+  P.hist_offset = P.vals_offset + ((8 * per_cta + 15) & ~15);
+  const int smem = P.hist_offset + 8 * (P.max_iter + 1);
+  if (smem > c->info.max_smem) return fail(BRM_EINVAL, "probe solve needs %d B of shared memory", smem);
+  BRM_TRY(allow_smem(c->kern.iz, smem));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(n * csize));
+  cfg.blockDim = dim3(kWalkThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = call.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void *args[] = {&P};
+  BRM_CUDA(cudaLaunchKernelExC(&cfg, c->kern.iz, args));
+  return call.finish();
+}
+
+}  // extern "C"

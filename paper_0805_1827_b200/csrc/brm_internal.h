@@ -1,0 +1,94 @@
+// brm_internal.h -- kernel parameter blocks shared by the kernels and the C ABI.
+#pragma once
+#include <cstdint>
+
+#include "brm_model.cuh"
+
+namespace brm {
+
+constexpr int kWalkThreads = 256;   // threads per walker CTA
+constexpr int kPathBlock = 4096;    // pricer.py:32 PATH_BLOCK (stream convention)
+constexpr int kPriceChunk = 1024;   // paths per pricing work item (4 per block)
+constexpr int kMaxChunk = 4096;     // largest chunk a walker CTA folds in smem
+
+struct WalkParams {
+  ModelHdr hdr;
+  const unsigned char *blob;
+  int n_units, per_unit, chunk, chunks_per_unit, n_items;
+  int64_t total_paths;
+  int m_start, n_steps;
+  const double *starts;  // [u * start_stride + i]; nullptr -> s0
+  int start_stride;
+  const uint64_t *keys, *streams;  // nullptr -> derive(seed, phase, item_base + u, key_date)
+  uint64_t seed;
+  int phase, key_date;
+  int64_t item_base;
+  uint64_t draw_base;
+  const double *normals;
+  uint64_t nrm_base, nrm_count;
+  int vals_offset;  // byte offset of the per-path value buffer in dynamic smem
+  double *partials;  // [n_items][2]
+  double *path_out;  // optional [n_units * per_unit]
+  int32_t *stop_out;
+};
+
+struct FinishParams {
+  const double *partials;
+  int n_units, chunks_per_unit, per_unit, mode;
+  int64_t total_paths;
+  const double *points;  // mode 2
+  int d, payoff;
+  double strike;
+  double *out;
+};
+
+struct IzParams {
+  ModelHdr hdr;
+  const unsigned char *blob;
+  int n_probes, m, n_steps, n_inner;
+  int solver;
+  double eps;
+  int max_iter, avg_window;
+  double lo, hi, tol;
+  const double *seeds;
+  int seed_stride;
+  const int32_t *assets;
+  const uint64_t *keys, *streams;
+  uint64_t seed;
+  int64_t item_base;
+  const double *normals;
+  uint64_t nrm_base, nrm_count;
+  int vals_offset, hist_offset;
+  double *out_level;
+  int32_t *out_iter, *out_conv;
+};
+
+struct DecisionParams {
+  ModelHdr hdr;
+  const unsigned char *blob;
+  const double *states;
+  int64_t n;
+  int m;
+  int32_t *out;
+};
+
+struct SampleParams {
+  int mode, m, d, n_dates;
+  uint64_t seed;
+  int64_t item_lo, n;
+  const double *s0, *chol, *step_mu, *step_vol, *bridge;
+  double *out;
+};
+
+struct KernelTriple {
+  void *walk, *iz, *dec;
+};
+
+KernelTriple kernels_for(int d, bool fast);
+int set_error(int code, const char *fmt, ...);
+void *finish_kernel();
+void *sample_kernel();
+void *fill_raw_kernel();
+void *fill_normals_kernel();
+
+}  // namespace brm

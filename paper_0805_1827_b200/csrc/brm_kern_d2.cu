@@ -1,0 +1,9 @@
+// Instantiation of the dimension-templated kernels for d = 2.
+#include "brm_kernels.cuh"
+
+namespace brm {
+KernelTriple kernels_d2(bool fast) {
+  if (fast) return KernelTriple{(void *)&walk_units<2, true>, (void *)&iz_probes<2, true>, (void *)&decisions<2, true>};
+  return KernelTriple{(void *)&walk_units<2, false>, (void *)&iz_probes<2, false>, (void *)&decisions<2, false>};
+}
+}  // namespace brm

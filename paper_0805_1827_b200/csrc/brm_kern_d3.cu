@@ -1,0 +1,9 @@
+// Instantiation of the dimension-templated kernels for d = 3.
+#include "brm_kernels.cuh"
+
+namespace brm {
+KernelTriple kernels_d3(bool fast) {
+  if (fast) return KernelTriple{(void *)&walk_units<3, true>, (void *)&iz_probes<3, true>, (void *)&decisions<3, true>};
+  return KernelTriple{(void *)&walk_units<3, false>, (void *)&iz_probes<3, false>, (void *)&decisions<3, false>};
+}
+}  // namespace brm

@@ -1,0 +1,9 @@
+// Instantiation of the dimension-templated kernels for d = 40.
+#include "brm_kernels.cuh"
+
+namespace brm {
+KernelTriple kernels_d40(bool fast) {
+  if (fast) return KernelTriple{(void *)&walk_units<40, true>, (void *)&iz_probes<40, true>, (void *)&decisions<40, true>};
+  return KernelTriple{(void *)&walk_units<40, false>, (void *)&iz_probes<40, false>, (void *)&decisions<40, false>};
+}
+}  // namespace brm

@@ -1,0 +1,9 @@
+// Instantiation of the dimension-templated kernels for d = 5.
+#include "brm_kernels.cuh"
+
+namespace brm {
+KernelTriple kernels_d5(bool fast) {
+  if (fast) return KernelTriple{(void *)&walk_units<5, true>, (void *)&iz_probes<5, true>, (void *)&decisions<5, true>};
+  return KernelTriple{(void *)&walk_units<5, false>, (void *)&iz_probes<5, false>, (void *)&decisions<5, false>};
+}
+}  // namespace brm

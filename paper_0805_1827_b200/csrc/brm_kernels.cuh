@@ -1,0 +1,245 @@
+// brm_kernels.cuh -- sm_100a kernels of the nested-MC engine (templates).
+//
+//   walk_units   persistent CTAs over (unit, chunk) work items; a unit is a
+//                pricing block (pricer.py:154-164), a CMC training point
+//                (_core.pyx:515-550) or a stopped_sums call (_core.pyx:402-430)
+//   finish_units fixed-order fold of chunk partials -> unit sums / labels
+//   iz_probes    one thread-block cluster per I&Z probe: the cluster's CTAs
+//                split the inner paths, reduce through distributed shared
+//                memory and iterate the fixed-point or bisection solve
+//                without leaving the kernel (_core.pyx:433-512)
+//   decisions, sample_points, raw/normal fills, key derivation
+#pragma once
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <type_traits>
+
+#include "brm_internal.h"
+#include "brm_walk.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace brm {
+
+// ---------------------------------------------------------------- walk ----
+template <int D, bool FAST>
+__global__ void __launch_bounds__(kWalkThreads) walk_units(WalkParams P) {
+  using R = RealT<FAST>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double s_red[2 * (kWalkThreads / 32)];
+  __shared__ int s_next;
+  __shared__ R s_start[kMaxD];
+  const Model<R> M = load_model<R>(P.hdr, P.blob, smem);
+  double *vals = reinterpret_cast<double *>(smem + P.vals_offset);
+  const int d = M.d;
+  const NormalSrc ns{P.normals, P.nrm_base, P.nrm_count};
+
+  for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+    const int u = item / P.chunks_per_unit;
+    const int c = item - u * P.chunks_per_unit;
+    const int64_t cnt64 = P.total_paths - (int64_t)u * P.per_unit;
+    const int cnt = (int)(cnt64 < P.per_unit ? cnt64 : P.per_unit);
+    const int p0 = c * P.chunk;
+    const int p1 = min(p0 + P.chunk, cnt);
+    uint64_t key, stream;
+    if (P.keys) {
+      key = P.keys[u];
+      stream = P.streams[u];
+    } else {
+      derive_words(P.seed, (uint64_t)P.phase, (uint64_t)(P.item_base + u), (uint64_t)P.key_date, key, stream);
+    }
+    __syncthreads();  // previous item finished with s_start / vals / s_next
+    if (threadIdx.x < d) s_start[threadIdx.x] = P.starts ? (R)P.starts[(size_t)u * P.start_stride + threadIdx.x]
+                                                         : M.s0[threadIdx.x];
+    if (threadIdx.x == 0) s_next = p0 + blockDim.x;
+    __syncthreads();
+    if (p0 < p1) {
+      const uint64_t base0 = unit_base<FAST>(P.draw_base, P.normals != nullptr);
+      double *pout = P.path_out ? P.path_out + (size_t)u * P.per_unit : nullptr;
+      int32_t *sout = P.stop_out ? P.stop_out + (size_t)u * P.per_unit : nullptr;
+      walk_paths<D, FAST>(M, s_start, P.m_start, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, pout,
+                          sout);
+    }
+    __syncthreads();
+    double s = 0.0, q = 0.0;
+    fold_values(vals, p1 > p0 ? p1 - p0 : 0, s_red, s, q);
+    if (threadIdx.x == 0) {
+      P.partials[2 * (size_t)item] = s;
+      P.partials[2 * (size_t)item + 1] = q;
+    }
+  }
+}
+
+// ------------------------------------------------------------ I&Z probes ----
+// Probe state for the payoff-driving scalar x (_core.pyx:476-483): the probed
+// asset at x, other assets at their seeds pulled to x - 0.01K when above x.
+// iz_space 1 (geometric put) sets the last asset so the state's geometric
+// mean is x.  Returns the probed asset's price.
+__device__ inline double probe_state(const ModelHdr &h, const double *seed, int asset, double x, double *st) {
+  const int d = h.d;
+  if (h.iz_space == 1) {
+    double sl = 0.0;
+    for (int j = 0; j < d - 1; ++j) {
+      st[j] = seed[j];
+      sl = __dadd_rn(sl, log(seed[j]));
+    }
+    st[d - 1] = exp(__dsub_rn(__dmul_rn((double)d, log(x)), sl));
+    return st[d - 1];
+  }
+  int j = 0;
+  for (int i = 0; i < d; ++i) {
+    if (i == asset) {
+      st[i] = x;
+    } else {
+      st[i] = seed[j] <= x ? seed[j] : __dsub_rn(x, __dmul_rn(0.01, h.strike));
+      ++j;
+    }
+  }
+  return x;
+}
+
+template <int D, bool FAST>
+__global__ void __launch_bounds__(kWalkThreads) iz_probes(IzParams P) {
+  using R = RealT<FAST>;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int csize = (int)cluster.num_blocks();
+  const int probe = blockIdx.x / csize;
+
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double s_red[2 * (kWalkThreads / 32)];
+  __shared__ int s_next;
+  __shared__ R s_start[kMaxD];
+  __shared__ double s_state[kMaxD];
+  __shared__ double s_part;                 // this CTA's partial sum
+  __shared__ double s_x, s_lo, s_hi;        // rank 0: solver state
+  __shared__ int s_done, s_it, s_armed, s_conv;
+  const Model<R> M = load_model<R>(P.hdr, P.blob, smem);
+  double *vals = reinterpret_cast<double *>(smem + P.vals_offset);
+  double *hist = reinterpret_cast<double *>(smem + P.hist_offset);
+  const int d = P.hdr.d;
+  const NormalSrc ns{P.normals, P.nrm_base, P.nrm_count};
+  const double K = P.hdr.strike;
+  const bool call_like = P.hdr.call_like != 0;
+
+  uint64_t key, stream;
+  if (P.keys) {
+    key = P.keys[probe];
+    stream = P.streams[probe];
+  } else {
+    derive_words(P.seed, 1 /* IZ_CALC */, (uint64_t)(P.item_base + probe), (uint64_t)P.m, key, stream);
+  }
+  const double *seedp = P.seeds + (size_t)probe * P.seed_stride;
+  const int asset = P.assets ? P.assets[probe] : 0;
+  const int per_cta = (P.n_inner + csize - 1) / csize;
+  const int p0 = rank * per_cta;
+  const int p1 = min(p0 + per_cta, P.n_inner);
+  const uint64_t per_path = (uint64_t)P.n_steps * (uint64_t)d;
+  const uint64_t slab = (uint64_t)P.n_inner * per_path;
+
+  if (threadIdx.x == 0 && rank == 0) {
+    s_x = P.solver == 0 ? K : 0.5 * (P.lo + P.hi);
+    s_lo = P.lo;
+    s_hi = P.hi;
+    s_done = P.solver == 1 ? !(P.hi - P.lo > P.tol && P.max_iter > 0) : (P.max_iter <= 0);
+    s_it = 0;
+    s_armed = 0;
+    s_conv = 0;
+    hist[0] = K;
+  }
+  cluster.sync();
+  double *x_remote = cluster.map_shared_rank(&s_x, 0);
+  int *done_remote = cluster.map_shared_rank(&s_done, 0);
+
+  for (int it = 0;; ++it) {
+    if (*done_remote) break;
+    const double x = *x_remote;
+    if (threadIdx.x == 0) probe_state(P.hdr, seedp, asset, x, s_state);
+    __syncthreads();
+    if (threadIdx.x < d) s_start[threadIdx.x] = (R)s_state[threadIdx.x];
+    if (threadIdx.x == 0) s_next = p0 + blockDim.x;
+    __syncthreads();
+    // fixed point: fresh slab per iteration; bisection: common random numbers
+    const uint64_t draw_base = P.solver == 0 ? (uint64_t)it * slab : 0;
+    const uint64_t base0 = unit_base<FAST>(draw_base, P.normals != nullptr);
+    if (p0 < p1)
+      walk_paths<D, FAST>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, nullptr,
+                          nullptr);
+    __syncthreads();
+    double s = 0.0, q = 0.0;
+    fold_values(vals, p1 > p0 ? p1 - p0 : 0, s_red, s, q);
+    if (threadIdx.x == 0) s_part = s;
+    cluster.sync();
+    if (rank == 0 && threadIdx.x == 0) {
+      double total = 0.0;
+      for (int r = 0; r < csize; ++r) total = __dadd_rn(total, *cluster.map_shared_rank(&s_part, r));
+      const double cont = __ddiv_rn(total, (double)P.n_inner);
+      const int n_it = it + 1;
+      s_it = n_it;
+      if (P.solver == 0) {
+        const double xn = call_like ? __dadd_rn(K, cont) : __dsub_rn(K, cont);
+        const double step = __dsub_rn(xn, x);
+        if (!s_armed && (call_like ? step <= 0.0 : step >= 0.0)) s_armed = 1;
+        s_x = xn;
+        hist[n_it] = xn;
+        if (s_armed && fabs(step) < P.eps) {
+          s_conv = 1;
+          s_done = 1;
+        } else if (n_it >= P.max_iter) {
+          s_done = 1;
+        }
+      } else {
+        double pay;
+        {
+          Model<double> Md{};
+          Md.d = d;
+          Md.payoff = P.hdr.payoff;
+          Md.strike = K;
+          pay = payoff<0>(Md, s_state);
+        }
+        const bool exercise = __dsub_rn(pay, cont) > 0.0;
+        if (call_like == exercise) s_hi = x;
+        else s_lo = x;
+        s_x = __dmul_rn(0.5, __dadd_rn(s_lo, s_hi));
+        if (!(__dsub_rn(s_hi, s_lo) > P.tol) || n_it >= P.max_iter) s_done = 1;
+      }
+    }
+    cluster.sync();
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    double level;
+    if (P.solver == 0) {
+      const int n_it = s_it;
+      const int n_avg = P.avg_window < n_it + 1 ? P.avg_window : n_it + 1;
+      double acc = 0.0;
+      for (int i = n_it + 1 - n_avg; i <= n_it; ++i) acc = __dadd_rn(acc, hist[i]);
+      level = __ddiv_rn(acc, (double)n_avg);
+    } else {
+      level = __dmul_rn(0.5, __dadd_rn(s_lo, s_hi));
+    }
+    double st[kMaxD];
+    P.out_level[probe] = probe_state(P.hdr, seedp, asset, level, st);
+    P.out_iter[probe] = s_it;
+    P.out_conv[probe] = P.solver == 0 ? s_conv : !(__dsub_rn(s_hi, s_lo) > P.tol);
+  }
+  cluster.sync();  // keep rank 0's shared memory alive until every CTA is done reading it
+}
+
+// ------------------------------------------------------------- decisions ----
+template <int D, bool FAST>
+__global__ void __launch_bounds__(256) decisions(DecisionParams P) {
+  using R = RealT<FAST>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Model<R> M = load_model<R>(P.hdr, P.blob, smem);
+  __syncthreads();
+  const int d = M.d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * blockDim.x) {
+    R v[D > 0 ? D : kMaxD];
+    #pragma unroll
+    for (int a = 0; a < dim_of<D>(d); ++a) v[a] = (R)P.states[i * d + a];
+    const R pay = payoff<D>(M, v);
+    P.out[i] = (pay > (R)0 && rule_stop<D>(M, P.m, v)) ? 1 : 0;
+  }
+}
+
+}  // namespace brm

@@ -1,0 +1,163 @@
+// brm_walk.cuh -- the lane-refilling path walker shared by every kernel.
+//
+// A CTA walks the paths [p0, p1) of one work unit (a pricing block, a CMC
+// training point, one I&Z probe iteration).  Each lane walks one path at a
+// time; when its path stops (or expires) the lane writes the discounted value
+// into shared memory at the path's slot and takes the next unclaimed path
+// from a CTA-wide counter (one atomic per warp per refill), so lanes never
+// idle behind a long path of a warp-mate.  Because values land at their path
+// slot, the chunk's (sum, sum of squares) is then folded in a fixed order and
+// is bit-identical run to run whatever the lane schedule was.
+#pragma once
+#include "brm_model.cuh"
+
+namespace brm {
+
+struct NormalSrc {
+  const double *ptr;  // supplied normals (fixed-input mode) or nullptr
+  uint64_t base, count;
+};
+
+__device__ __forceinline__ double supplied_normal(const NormalSrc &s, uint64_t idx) {
+  const uint64_t off = idx - s.base;
+  return off < s.count ? s.ptr[off] : __longlong_as_double(0x7ff8000000000000LL);
+}
+
+template <bool FAST>
+using RealT = typename std::conditional<FAST, float, double>::type;
+
+// Draws of step k of a path: parity indices base + k*d + a (reference
+// _core.pyx:4-7); fast positions pos + k*dp + a.
+template <int D, bool FAST>
+__device__ __forceinline__ void path_step_draws(int d, uint64_t key, uint64_t stream, uint64_t base, int k,
+                                                const NormalSrc &ns, RealT<FAST> *z) {
+  if (ns.ptr) {
+    const uint64_t idx0 = base + (uint64_t)k * (uint64_t)d;
+#pragma unroll
+    for (int a = 0; a < dim_of<D>(d); ++a) z[a] = (RealT<FAST>)supplied_normal(ns, idx0 + a);
+    return;
+  }
+  if constexpr (FAST) {
+    const int dp = d + (d & 1);
+    step_draws_fast<D>(key, stream, base + (uint64_t)k * (uint64_t)dp, z, d);
+  } else {
+    step_draws<D>(key, stream, base + (uint64_t)k * (uint64_t)d, z, d);
+  }
+}
+
+// Stride (in draw indices / positions) between consecutive paths of a unit.
+template <bool FAST>
+__host__ __device__ __forceinline__ uint64_t path_stride(int d, int n_steps, bool supplied) {
+  if (FAST && !supplied) return (uint64_t)n_steps * (uint64_t)(d + (d & 1));
+  return (uint64_t)n_steps * (uint64_t)d;
+}
+
+// First draw index / position of a unit that starts at parity draw_base.
+// Fast mode starts at the first Philox call not touched by parity draws
+// [0, draw_base), so sampler draws and path draws never share a counter.
+template <bool FAST>
+__host__ __device__ __forceinline__ uint64_t unit_base(uint64_t draw_base, bool supplied) {
+  if (FAST && !supplied) return 2 * (draw_base + (draw_base & 1));
+  return draw_base;
+}
+
+// Walk paths [p0, p1) of one unit from the shared start state.  *s_next must
+// hold p0 + blockDim.x (set by the caller, followed by __syncthreads()).
+template <int D, bool FAST>
+__device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_start, int m_start, int n_steps,
+                           uint64_t key, uint64_t stream, uint64_t base0, int p0, int p1, const NormalSrc &ns,
+                           double *vals, int *s_next, double *path_out, int32_t *stop_out) {
+  using R = RealT<FAST>;
+  const int d = dim_of<D>(M.d);
+  const uint64_t stride = path_stride<FAST>(d, n_steps, ns.ptr != nullptr);
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  constexpr int NV = D > 0 ? D : kMaxD;
+  R v[NV], z[NV];
+
+  int p = p0 + threadIdx.x;
+  bool have = p < p1;
+  int k = 0;
+  uint64_t base = base0 + (uint64_t)(have ? p : 0) * stride;
+#pragma unroll
+  for (int i = 0; i < dim_of<D>(d); ++i) v[i] = s_start[i];
+
+  while (__any_sync(0xffffffffu, have)) {
+    bool done = false;
+    double val = 0.0;
+    int stop_m = 0;
+    if (have) {
+      path_step_draws<D, FAST>(d, key, stream, base, k, ns, z);
+      gbm_step<D>(M, v, z);
+      const int m = m_start + k + 1;
+      const R pay = payoff<D>(M, v);
+      if (pay > (R)0 && rule_stop<D>(M, m, v)) {
+        val = (double)pay * M.disc[m - m_start];
+        stop_m = m;
+        done = true;
+      } else if (k + 1 == n_steps) {
+        done = true;
+      } else {
+        ++k;
+      }
+    }
+    if (done) {
+      vals[p - p0] = val;
+      if (path_out) path_out[p] = val;
+      if (stop_out) stop_out[p] = stop_m;
+    }
+    const unsigned need = __ballot_sync(0xffffffffu, done);
+    if (need) {
+      const int leader = __ffs(need) - 1;
+      int got = 0;
+      if ((int)lane == leader) got = atomicAdd(s_next, __popc(need));
+      got = __shfl_sync(0xffffffffu, got, leader);
+      if (done) {
+        p = got + __popc(need & lt_mask);
+        have = p < p1;
+        k = 0;
+        base = base0 + (uint64_t)(have ? p : 0) * stride;
+#pragma unroll
+        for (int i = 0; i < dim_of<D>(d); ++i) v[i] = s_start[i];
+      }
+    }
+  }
+}
+
+// Fixed-order fold of vals[0..n) into (sum, sumsq); result valid in thread 0.
+// Thread t folds a contiguous run, then a shuffle tree and a warp-order pass.
+__device__ inline void fold_values(const double *vals, int n, double *s_red, double &sum, double &sumsq) {
+  const int nt = blockDim.x;
+  const int per = (n + nt - 1) / nt;
+  const int lo = threadIdx.x * per;
+  const int hi = min(lo + per, n);
+  double s = 0.0, q = 0.0;
+  for (int i = lo; i < hi; ++i) {
+    const double x = vals[i];
+    s = __dadd_rn(s, x);
+    q = __dadd_rn(q, __dmul_rn(x, x));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
+    q = __dadd_rn(q, __shfl_down_sync(0xffffffffu, q, off));
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_red[2 * warp] = s;
+    s_red[2 * warp + 1] = q;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s = 0.0;
+    q = 0.0;
+    for (int w = 0; w < (nt + 31) / 32; ++w) {
+      s = __dadd_rn(s, s_red[2 * w]);
+      q = __dadd_rn(q, s_red[2 * w + 1]);
+    }
+    sum = s;
+    sumsq = q;
+  }
+}
+
+}  // namespace brm
