@@ -166,22 +166,55 @@ int brm_iz_solve(brm_ctx *ctx, int32_t solver, const double *seeds, const int32_
                  double hi, double tol, const uint64_t *keys, const uint64_t *streams, uint64_t seed,
                  int64_t item_lo, double *out_level, int32_t *out_iterations, int32_t *out_converged);
 
+/* ---- CMC date step: sampler + features + labels (boundary_cmc.py:210-227) */
+/* Items [item_lo, item_lo+n) of date m: sample the training point (sampler
+ * 0 = reference bridge, 1 = forward; bridge as in brm_sample_points), write
+ * its classifier features out_features[i*F + f] with F = d+1 for d>1 (the
+ * d prices plus the payoff aggregate: max for the max-call as the reference's
+ * classifier_features, boundary_cmc.py:38-52; arithmetic / geometric mean for
+ * the basket / geometric puts) and F = 1 for d = 1, and its label
+ * out_beta[i] = payoff - continuation with n_label paths under the
+ * context's (later-dates) rule, continuing the point's stream after the
+ * sampler draws. */
+int brm_cmc_calc(brm_ctx *ctx, int32_t sampler, int32_t m, uint64_t seed, int64_t item_lo, int64_t n,
+                 int32_t n_label, const double *bridge, double *out_features, double *out_beta);
+
 /* ---- AdaBoost stumps (boosting.py:126-206) ------------------------------ */
-/* xs [n*F] row-major features, betas [n] (y = +1 iff beta > 0).  mode
- * BRM_MODE_PARITY replays numpy's summation orders (sequential cumsum,
- * pairwise sum) and the reference tie rules; BRM_MODE_FAST uses exact
- * fixed-point weight scans.  Outputs sized [rounds]; *out_count stumps
- * picked; *out_intercept the ensemble intercept. */
-int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, const double *betas, int64_t n,
-                     int32_t F, int32_t rounds, int32_t *out_feat, double *out_thr, double *out_pol,
-                     double *out_alpha, int32_t *out_count, double *out_intercept);
+/* xs [n*F] row-major features, betas [n] (y = +1 iff beta > 0), weights [n]
+ * initial weights or NULL for 1/n.  BRM_MODE_PARITY replays numpy's
+ * summation orders (sequential cumsum, pairwise sum) and the reference tie
+ * rules.  flags BRM_FIT_SINGLE_STUMP: one fit_stump search (boosting.py:
+ * 126-171) with the given weights, no boosting rules.  Outputs sized
+ * [rounds]; *out_count stumps picked; out_err the weighted error of each;
+ * *out_intercept the ensemble intercept.  stream: cudaStream_t or NULL. */
+#define BRM_FIT_SINGLE_STUMP 1
+int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, void *stream, const double *xs,
+                     const double *betas, const double *weights, int64_t n, int32_t F, int32_t rounds,
+                     int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha, double *out_err,
+                     int32_t *out_count, double *out_intercept);
 
 /* ---- Quadratic boundary regression (boundary_iz.py:250-276) ------------- */
-/* Least squares over the design [n*nb] (row-major), fp64 Householder QR on
- * the device; rank-deficient designs fall back to the cross-term-free basis
- * (zeros in dropped columns).  *out_rank_deficient set to 1 on fallback. */
-int brm_lstsq(int32_t device, const double *design, const double *levels, int64_t n, int32_t nb,
+/* Least squares over the design [n*nb] (row-major), fp64 Householder QR with
+ * column pivoting on the device; rank-deficient designs fall back to the
+ * cross-term-free basis over k coordinates (zeros in dropped columns) and set
+ * *out_rank_deficient. */
+int brm_lstsq(int32_t device, void *stream, const double *design, const double *levels, int64_t n, int32_t nb,
               int32_t k_coords, double *out_coeffs, int32_t *out_rank_deficient);
+
+/* ---- Launch accounting (bench.py) -------------------------------------- */
+/* Kernel families: 0 walker (pricing / labels / stopped_sums), 1 probe
+ * clusters, 2 AdaBoost, 3 sampler, 4 unit fold, 5 lstsq, 6 RNG fills,
+ * 7 decisions, 8 auxiliary.  Launches are always counted; with profiling
+ * enabled every launch is bracketed by CUDA events on its stream.
+ * path_steps counts path-steps executed by walker / probe kernels. */
+enum brm_prof_kind { BRM_PROF_WALK = 0, BRM_PROF_IZ = 1, BRM_PROF_BOOST = 2, BRM_PROF_SAMPLE = 3,
+                     BRM_PROF_FINISH = 4, BRM_PROF_LSTSQ = 5, BRM_PROF_RNG = 6, BRM_PROF_DEC = 7,
+                     BRM_PROF_AUX = 8, BRM_PROF_KINDS = 9 };
+int brm_profile_enable(int32_t on);
+int brm_profile_reset(void);
+int brm_profile_read(int32_t kind, double *ms, uint64_t *launches, uint64_t *path_steps);
+/* Host<->device bytes staged by the library since the last brm_profile_reset. */
+int brm_transfer_read(uint64_t *h2d_bytes, uint64_t *d2h_bytes);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

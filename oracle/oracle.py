@@ -362,3 +362,29 @@ def cpu_count() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------- lattice ----
+def crr_bermudan(s0, strike, r, delta, sigma, maturity, n_dates, steps, put=True):
+    """CRR lattice Bermudan price, exercise at n_dates equally spaced dates
+    (restates the reference's crr_price, oracle.py:98-143, for d = 1)."""
+    import math
+    dt = maturity / steps
+    u = math.exp(sigma * math.sqrt(dt))
+    dn = 1.0 / u
+    p = (math.exp((r - delta) * dt) - dn) / (u - dn)
+    if not 0.0 < p < 1.0:
+        raise ValueError("risk-neutral probability outside (0, 1)")
+    disc = math.exp(-r * dt)
+    stride = steps // n_dates
+    ex = {stride * m for m in range(1, n_dates + 1)}
+
+    def intrinsic(s):
+        return np.maximum(strike - s, 0.0) if put else np.maximum(s - strike, 0.0)
+
+    vals = intrinsic(s0 * u ** (2.0 * np.arange(steps + 1) - steps))
+    for i in range(steps - 1, -1, -1):
+        vals = disc * (p * vals[1:i + 2] + (1.0 - p) * vals[:i + 1])
+        if i in ex:
+            vals = np.maximum(vals, intrinsic(s0 * u ** (2.0 * np.arange(i + 1) - i)))
+    return float(vals[0])

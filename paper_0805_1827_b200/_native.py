@@ -18,6 +18,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "lib" / "libbermuda_b200.so"
 
 BRM_OK, BRM_EINVAL, BRM_ENOMEM, BRM_ECUDA, BRM_ENODEV = range(5)
 MODE_PARITY, MODE_FAST = 0, 1
+FIT_SINGLE_STUMP = 1
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -67,10 +68,17 @@ _SIGNATURES = {
                                C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
                                C.c_void_p, C.c_void_p, C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p,
                                C.c_void_p]),
-    "brm_fit_ensemble": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
-                                   C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, _ip, _dp]),
-    "brm_lstsq": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
-                            _ip]),
+    "brm_cmc_calc": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int32,
+                               C.c_void_p, C.c_void_p, C.c_void_p]),
+    "brm_fit_ensemble": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, _ip, _dp]),
+    "brm_profile_enable": (C.c_int, [C.c_int32]),
+    "brm_profile_reset": (C.c_int, []),
+    "brm_profile_read": (C.c_int, [C.c_int32, _dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "brm_transfer_read": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "brm_lstsq": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
+                            C.c_void_p, _ip]),
 }
 
 
@@ -121,7 +129,41 @@ def f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+def stream_handle(stream) -> C.c_void_p | None:
+    """cudaStream_t of a torch.cuda.Stream / raw int / None (legacy default stream)."""
+    raw = getattr(stream, "cuda_stream", stream)
+    return C.c_void_p(raw) if raw else None
+
+
 def device_count() -> int:
     n = C.c_int32(0)
     st = lib.brm_device_count(C.byref(n))
     return int(n.value) if st == BRM_OK else 0
+
+
+PROF_KINDS = ("walk", "iz", "boost", "sample", "finish", "lstsq", "rng", "decisions", "aux")
+
+
+def profile_read() -> dict:
+    """{family: (device ms, launches, executed path-steps)} since the last reset."""
+    out = {}
+    for i, name in enumerate(PROF_KINDS):
+        ms, nl, ns = C.c_double(), C.c_uint64(), C.c_uint64()
+        check(lib.brm_profile_read(i, C.byref(ms), C.byref(nl), C.byref(ns)))
+        out[name] = (ms.value, int(nl.value), int(ns.value))
+    return out
+
+
+def transfer_read() -> tuple[int, int]:
+    """(host->device, device->host) bytes staged by the library since the last reset."""
+    a, b = C.c_uint64(), C.c_uint64()
+    check(lib.brm_transfer_read(C.byref(a), C.byref(b)))
+    return int(a.value), int(b.value)
+
+
+def profile_enable(on: bool = True) -> None:
+    check(lib.brm_profile_enable(1 if on else 0))
+
+
+def profile_reset() -> None:
+    check(lib.brm_profile_reset())

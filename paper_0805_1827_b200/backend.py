@@ -184,29 +184,51 @@ def price_blocks(mp, rp, n_paths: int, seed: int, block_lo: int = 0, block_hi: i
     return out
 
 
-def fit_ensemble_arrays(xs, betas, rounds: int, mode=None, device=None):
-    """Device AdaBoost (boosting.py:174-206) -> (feat, thr, pol, alpha, intercept) arrays."""
+def fit_ensemble_arrays(xs, betas, rounds: int, mode=None, device=None, weights=None, single: bool = False,
+                        stream=None):
+    """Device AdaBoost (boosting.py:174-206) -> (feat, thr, pol, alpha, err, intercept) arrays.
+
+    ``single`` runs one fit_stump search (boosting.py:126-171) with ``weights``."""
     from .context import resolve_mode
     xs = xs if not isinstance(xs, np.ndarray) else N.f64(xs)
     betas = betas if not isinstance(betas, np.ndarray) else N.f64(betas)
+    w = None if weights is None else (weights if not isinstance(weights, np.ndarray) else N.f64(weights))
     n, F = int(xs.shape[0]), int(xs.shape[1])
-    feat = np.empty(rounds, dtype=np.int32)
-    thr, pol, alpha = np.empty(rounds), np.empty(rounds), np.empty(rounds)
+    r = 1 if single else int(rounds)
+    feat = np.empty(r, dtype=np.int32)
+    thr, pol, alpha, err = np.empty(r), np.empty(r), np.empty(r), np.empty(r)
     count, icept = C.c_int32(), C.c_double()
-    N.check(N.lib.brm_fit_ensemble(_dev(device), resolve_mode(mode), N.ptr(xs), N.ptr(betas), n, F, int(rounds),
-                                   N.ptr(feat), N.ptr(thr), N.ptr(pol), N.ptr(alpha), C.byref(count),
+    N.check(N.lib.brm_fit_ensemble(_dev(device), resolve_mode(mode), N.FIT_SINGLE_STUMP if single else 0,
+                                   N.stream_handle(stream), N.ptr(xs), N.ptr(betas), N.ptr(w), n, F, r,
+                                   N.ptr(feat), N.ptr(thr), N.ptr(pol), N.ptr(alpha), N.ptr(err), C.byref(count),
                                    C.byref(icept)))
     c = count.value
-    return feat[:c], thr[:c], pol[:c], alpha[:c], float(icept.value)
+    return feat[:c], thr[:c], pol[:c], alpha[:c], err[:c], float(icept.value)
 
 
-def lstsq(design, levels, k_coords: int, device=None):
+def lstsq(design, levels, k_coords: int, device=None, stream=None):
     """Device least squares with the cross-term-free fallback (boundary_iz.py:250-276)."""
     design = N.f64(design)
     levels = N.f64(levels)
     n, nb = design.shape
     out = np.empty(nb)
     deficient = C.c_int32()
-    N.check(N.lib.brm_lstsq(_dev(device), N.ptr(design), N.ptr(levels), n, nb, int(k_coords), N.ptr(out),
-                            C.byref(deficient)))
+    N.check(N.lib.brm_lstsq(_dev(device), N.stream_handle(stream), N.ptr(design), N.ptr(levels), n, nb,
+                            int(k_coords), N.ptr(out), C.byref(deficient)))
     return out, bool(deficient.value)
+
+
+def cmc_calc(mp, rp, m: int, seed: int, item_lo: int, n: int, n_label: int, bridge=None, sampler: str = "bridge",
+             out_features=None, out_beta=None, mode=None, device=None):
+    """Sample, featurise and label training points [item_lo, item_lo+n) of date m on the device."""
+    ctx = get_context(mp, rp, device, mode)
+    d = int(mp.d)
+    F = d + 1 if d > 1 else 1
+    if out_features is None:
+        out_features = np.empty((int(n), F))
+    if out_beta is None:
+        out_beta = np.empty(int(n))
+    b = N.f64(bridge) if bridge is not None else None
+    N.check(N.lib.brm_cmc_calc(ctx.handle, {"bridge": 0, "forward": 1}[sampler], int(m), int(seed) & (2**64 - 1),
+                               int(item_lo), int(n), int(n_label), N.ptr(b), N.ptr(out_features), N.ptr(out_beta)))
+    return out_features, out_beta

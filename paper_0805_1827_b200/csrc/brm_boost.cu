@@ -165,8 +165,9 @@ struct BoostParams {
   int *feat_pos;           // [F] 2*i + (pol == -1)
   double *wsub;            // [F][n] per-CTA scratch for the constant-stump sums
   int *out_feat;
-  double *out_thr, *out_pol, *out_alpha;
+  double *out_thr, *out_pol, *out_alpha, *out_err;
   int *out_count;
+  int raw;  // 1: one fit_stump search with the given weights, no boosting rules
 };
 
 struct Cand {
@@ -319,7 +320,17 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
     // alpha = 0.5 * log((1 - err) / max(err, 1e-10)); stop rules of fit_ensemble
     if (threadIdx.x == 0) {
       const double err = s_alpha;
-      if (err >= 0.5) {
+      if (P.raw) {
+        // fit_stump semantics (boosting.py:126-171): best stump and its error only
+        if (blockIdx.x == 0) {
+          P.out_feat[0] = s_feat;
+          P.out_thr[0] = s_thr;
+          P.out_pol[0] = s_pol;
+          P.out_alpha[0] = 1.0;
+          P.out_err[0] = err;
+        }
+        s_stop = 3;
+      } else if (err >= 0.5) {
         s_stop = 1;
       } else {
         const double a = __dmul_rn(0.5, log(__ddiv_rn(__dsub_rn(1.0, err), err > 1e-10 ? err : 1e-10)));
@@ -329,6 +340,7 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
           P.out_thr[count] = s_thr;
           P.out_pol[count] = s_pol;
           P.out_alpha[count] = a;
+          P.out_err[count] = err;
         }
         s_stop = err <= 0.0 ? 3 : 0;
       }
@@ -503,24 +515,27 @@ bool is_dev(const void *p) {
     }                                                                                    \
   } while (0)
 
-extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, const double *betas, int64_t n64,
-                                int32_t F, int32_t rounds, int32_t *out_feat, double *out_thr, double *out_pol,
-                                double *out_alpha, int32_t *out_count, double *out_intercept) {
+extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, void *stream, const double *xs,
+                                const double *betas, const double *weights, int64_t n64, int32_t F, int32_t rounds,
+                                int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha,
+                                double *out_err, int32_t *out_count, double *out_intercept) {
   (void)mode;  // both modes replay numpy's summation orders in this build
+  const bool raw = flags & BRM_FIT_SINGLE_STUMP;
   if (!xs || !betas || !out_count || !out_intercept) return bfail(BRM_EINVAL, "NULL argument");
   if (rounds < 1) return bfail(BRM_EINVAL, "need at least one round, got " + std::to_string(rounds));
   if (n64 < 1 || n64 > (1 << 26)) return bfail(BRM_EINVAL, "training set size out of range");
   if (F < 1 || F > 148) return bfail(BRM_EINVAL, "feature count out of range");
-  if (rounds > 0 && (!out_feat || !out_thr || !out_pol || !out_alpha)) return bfail(BRM_EINVAL, "NULL stump outputs");
+  if (!out_feat || !out_thr || !out_pol || !out_alpha || !out_err) return bfail(BRM_EINVAL, "NULL stump outputs");
   const int n = (int)n64;
+  if (raw) rounds = 1;
   int rc = BRM_OK;
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  cudaStream_t s = nullptr;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   double *d_xs = nullptr, *d_b = nullptr, *d_xt = nullptr, *d_xsorted = nullptr, *d_y = nullptr, *d_w = nullptr;
   double *d_pc = nullptr, *d_nc = nullptr, *d_err = nullptr, *d_wsub = nullptr, *d_thr = nullptr, *d_pol = nullptr,
-         *d_alpha = nullptr;
+         *d_alpha = nullptr, *d_rerr = nullptr;
   int *d_iota = nullptr, *d_order = nullptr, *d_pos = nullptr, *d_npos = nullptr, *d_feat = nullptr,
       *d_count = nullptr;
   int2 *d_leaves = nullptr;
@@ -528,18 +543,23 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, 
   size_t tmp_bytes = 0;
   int npos = 0;
   std::vector<int2> leaves;
-  BCU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   BCU(cudaMallocAsync(&d_xs, sizeof(double) * (size_t)n * F, s));
-  BCU(cudaMemcpyAsync(d_xs, xs, sizeof(double) * (size_t)n * F, is_dev(xs) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  BCU(cudaMemcpyAsync(d_xs, xs, sizeof(double) * (size_t)n * F, cudaMemcpyDefault, s));
+  if (!is_dev(xs)) count_transfer(sizeof(double) * (size_t)n * F, 0);
+  if (!is_dev(betas)) count_transfer(sizeof(double) * n, 0);
   BCU(cudaMallocAsync(&d_b, sizeof(double) * n, s));
-  BCU(cudaMemcpyAsync(d_b, betas, sizeof(double) * n, is_dev(betas) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  BCU(cudaMemcpyAsync(d_b, betas, sizeof(double) * n, cudaMemcpyDefault, s));
   BCU(cudaMallocAsync(&d_y, sizeof(double) * n, s));
   BCU(cudaMallocAsync(&d_npos, sizeof(int), s));
   BCU(cudaMemsetAsync(d_npos, 0, sizeof(int), s));
-  labels_from_betas<<<(n + 255) / 256, 256, 0, s>>>(d_b, n, d_y, d_npos);
+  {
+    const int tok = prof_begin(PK_AUX, s);
+    labels_from_betas<<<(n + 255) / 256, 256, 0, s>>>(d_b, n, d_y, d_npos);
+    prof_end(tok, s);
+  }
   BCU(cudaMemcpyAsync(&npos, d_npos, sizeof(int), cudaMemcpyDeviceToHost, s));
   BCU(cudaStreamSynchronize(s));
-  if (npos == 0 || npos == n) {
+  if (!raw && (npos == 0 || npos == n)) {
     // one class: zero-round ensemble carrying the class sign (boosting.py:185-187)
     *out_count = 0;
     *out_intercept = npos == n ? 1.0 : -1.0;
@@ -549,14 +569,24 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, 
   BCU(cudaMallocAsync(&d_xsorted, sizeof(double) * (size_t)n * F, s));
   BCU(cudaMallocAsync(&d_iota, sizeof(int) * n, s));
   BCU(cudaMallocAsync(&d_order, sizeof(int) * (size_t)n * F, s));
-  transpose_cols<<<(unsigned)(((int64_t)n * F + 255) / 256), 256, 0, s>>>(d_xs, n, F, d_xt, d_iota);
+  {
+    const int tok = prof_begin(PK_AUX, s);
+    transpose_cols<<<(unsigned)(((int64_t)n * F + 255) / 256), 256, 0, s>>>(d_xs, n, F, d_xt, d_iota);
+    prof_end(tok, s);
+  }
   BCU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_xt, d_xsorted, d_iota, d_order, n, 0, 64, s));
   BCU(cudaMallocAsync(&d_tmp, tmp_bytes, s));
   for (int f = 0; f < F; ++f)
     BCU(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_xt + (size_t)f * n, d_xsorted + (size_t)f * n, d_iota,
                                         d_order + (size_t)f * n, n, 0, 64, s));
   BCU(cudaMallocAsync(&d_w, sizeof(double) * n, s));
-  fill_value<<<(n + 255) / 256, 256, 0, s>>>(d_w, n, 1.0 / n);
+  if (weights) {
+    BCU(cudaMemcpyAsync(d_w, weights, sizeof(double) * n, cudaMemcpyDefault, s));
+  } else {
+    const int tok = prof_begin(PK_AUX, s);
+    fill_value<<<(n + 255) / 256, 256, 0, s>>>(d_w, n, 1.0 / n);
+    prof_end(tok, s);
+  }
   BCU(cudaMallocAsync(&d_pc, sizeof(double) * (size_t)n * F, s));
   BCU(cudaMallocAsync(&d_nc, sizeof(double) * (size_t)n * F, s));
   BCU(cudaMallocAsync(&d_err, sizeof(double) * F, s));
@@ -566,6 +596,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, 
   BCU(cudaMallocAsync(&d_thr, sizeof(double) * rounds, s));
   BCU(cudaMallocAsync(&d_pol, sizeof(double) * rounds, s));
   BCU(cudaMallocAsync(&d_alpha, sizeof(double) * rounds, s));
+  BCU(cudaMallocAsync(&d_rerr, sizeof(double) * rounds, s));
   BCU(cudaMallocAsync(&d_count, sizeof(int), s));
   pw_leaves(0, n, leaves);
   BCU(cudaMallocAsync(&d_leaves, sizeof(int2) * leaves.size(), s));
@@ -575,6 +606,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, 
     P.n = n;
     P.F = F;
     P.rounds = rounds;
+    P.raw = raw ? 1 : 0;
     P.xs = d_xs;
     P.xsorted = d_xsorted;
     P.order = d_order;
@@ -591,11 +623,14 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, 
     P.out_thr = d_thr;
     P.out_pol = d_pol;
     P.out_alpha = d_alpha;
+    P.out_err = d_rerr;
     P.out_count = d_count;
     const size_t smem = sizeof(double) * (leaves.size() + 3 * kTile) + kTile;
     BCU(cudaFuncSetAttribute(boost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     void *args[] = {&P};
+    const int tok = prof_begin(PK_BOOST, s);
     BCU(cudaLaunchCooperativeKernel((void *)boost_kernel, dim3(F), dim3(kBoostThreads), args, smem, s));
+    prof_end(tok, s);
   }
   BCU(cudaGetLastError());
   {
@@ -604,13 +639,13 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, 
     BCU(cudaStreamSynchronize(s));
     *out_count = count;
     if (count > 0) {
-      std::vector<int> feat(count);
-      BCU(cudaMemcpy(feat.data(), d_feat, sizeof(int) * count, cudaMemcpyDeviceToHost));
-      BCU(cudaMemcpy(out_thr, d_thr, sizeof(double) * count, cudaMemcpyDefault));
-      BCU(cudaMemcpy(out_pol, d_pol, sizeof(double) * count, cudaMemcpyDefault));
-      BCU(cudaMemcpy(out_alpha, d_alpha, sizeof(double) * count, cudaMemcpyDefault));
-      BCU(cudaMemcpy(out_feat, feat.data(), sizeof(int) * count, cudaMemcpyDefault));
+      BCU(cudaMemcpyAsync(out_feat, d_feat, sizeof(int) * count, cudaMemcpyDefault, s));
+      BCU(cudaMemcpyAsync(out_thr, d_thr, sizeof(double) * count, cudaMemcpyDefault, s));
+      BCU(cudaMemcpyAsync(out_pol, d_pol, sizeof(double) * count, cudaMemcpyDefault, s));
+      BCU(cudaMemcpyAsync(out_alpha, d_alpha, sizeof(double) * count, cudaMemcpyDefault, s));
+      BCU(cudaMemcpyAsync(out_err, d_rerr, sizeof(double) * count, cudaMemcpyDefault, s));
       *out_intercept = 0.0;
+      count_transfer(0, (sizeof(int) + 4 * sizeof(double)) * count);
     } else {
       // no stump beat random guessing: majority sign (boosting.py:202-205)
       *out_intercept = 2 * npos >= n ? 1.0 : -1.0;
@@ -619,19 +654,16 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, const double *xs, 
 done:
   for (void *p : {(void *)d_xs, (void *)d_b, (void *)d_xt, (void *)d_xsorted, (void *)d_y, (void *)d_w, (void *)d_pc,
                   (void *)d_nc, (void *)d_err, (void *)d_wsub, (void *)d_thr, (void *)d_pol, (void *)d_alpha,
-                  (void *)d_iota, (void *)d_order, (void *)d_pos, (void *)d_npos, (void *)d_feat, (void *)d_count,
-                  (void *)d_leaves, d_tmp})
+                  (void *)d_rerr, (void *)d_iota, (void *)d_order, (void *)d_pos, (void *)d_npos, (void *)d_feat,
+                  (void *)d_count, (void *)d_leaves, d_tmp})
     if (p) cudaFreeAsync(p, s);
-  if (s) {
-    cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
-  }
+  cudaStreamSynchronize(s);
   if (prev >= 0) cudaSetDevice(prev);
   return rc;
 }
 
-extern "C" int brm_lstsq(int32_t device, const double *design, const double *levels, int64_t n64, int32_t nb,
-                         int32_t k, double *out_coeffs, int32_t *out_rank_deficient) {
+extern "C" int brm_lstsq(int32_t device, void *stream, const double *design, const double *levels, int64_t n64,
+                         int32_t nb, int32_t k, double *out_coeffs, int32_t *out_rank_deficient) {
   if (!design || !levels || !out_coeffs || !out_rank_deficient) return bfail(BRM_EINVAL, "NULL argument");
   if (nb < 1 || nb > kLsMaxB) return bfail(BRM_EINVAL, "basis size out of range");
   if (n64 < nb) return bfail(BRM_EINVAL, "need at least " + std::to_string(nb) + " probe points for the quadratic fit, got " + std::to_string(n64));
@@ -641,14 +673,13 @@ extern "C" int brm_lstsq(int32_t device, const double *design, const double *lev
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  cudaStream_t s = nullptr;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   double *d_design = nullptr, *d_levels = nullptr, *d_coeffs = nullptr;
   int *d_cols = nullptr, *d_rank = nullptr;
   std::vector<int> cols(nb);
   int rank = 0;
   for (int c = 0; c < nb; ++c) cols[c] = c;
   const size_t smem_full = sizeof(double) * ((size_t)nb * n + n);
-  BCU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   BCU(cudaMallocAsync(&d_design, sizeof(double) * (size_t)n * nb, s));
   BCU(cudaMemcpyAsync(d_design, design, sizeof(double) * (size_t)n * nb, cudaMemcpyDefault, s));
   BCU(cudaMallocAsync(&d_levels, sizeof(double) * n, s));
@@ -658,7 +689,11 @@ extern "C" int brm_lstsq(int32_t device, const double *design, const double *lev
   BCU(cudaMallocAsync(&d_rank, sizeof(int), s));
   BCU(cudaMemcpyAsync(d_cols, cols.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
   BCU(cudaFuncSetAttribute(lstsq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
-  lstsq_kernel<<<1, 256, smem_full, s>>>(d_design, d_levels, n, nb, d_cols, nb, d_coeffs, d_rank);
+  {
+    const int tok = prof_begin(PK_LSTSQ, s);
+    lstsq_kernel<<<1, 256, smem_full, s>>>(d_design, d_levels, n, nb, d_cols, nb, d_coeffs, d_rank);
+    prof_end(tok, s);
+  }
   BCU(cudaGetLastError());
   BCU(cudaMemcpyAsync(&rank, d_rank, sizeof(int), cudaMemcpyDeviceToHost, s));
   BCU(cudaStreamSynchronize(s));
@@ -673,8 +708,10 @@ extern "C" int brm_lstsq(int32_t device, const double *design, const double *lev
       pos += k - a;
     }
     BCU(cudaMemcpyAsync(d_cols, keep.data(), sizeof(int) * keep.size(), cudaMemcpyHostToDevice, s));
+    const int tok = prof_begin(PK_LSTSQ, s);
     lstsq_kernel<<<1, 256, sizeof(double) * (keep.size() * n + n), s>>>(d_design, d_levels, n, nb, d_cols,
                                                                         (int)keep.size(), d_coeffs, d_rank);
+    prof_end(tok, s);
     BCU(cudaGetLastError());
   }
   BCU(cudaMemcpyAsync(out_coeffs, d_coeffs, sizeof(double) * nb, cudaMemcpyDefault, s));
@@ -682,10 +719,7 @@ extern "C" int brm_lstsq(int32_t device, const double *design, const double *lev
 done:
   for (void *p : {(void *)d_design, (void *)d_levels, (void *)d_coeffs, (void *)d_cols, (void *)d_rank})
     if (p) cudaFreeAsync(p, s);
-  if (s) {
-    cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
-  }
+  cudaStreamSynchronize(s);
   if (prev >= 0) cudaSetDevice(prev);
   return rc;
 }

@@ -105,6 +105,7 @@ struct Call {
     a.owned = true;
     args.push_back(a);
     BRM_CUDA(cudaMemcpyAsync(a.dev, p, a.bytes, cudaMemcpyHostToDevice, stream));
+    count_transfer(a.bytes, 0);
     *out = static_cast<const T *>(a.dev);
     return BRM_OK;
   }
@@ -139,7 +140,10 @@ struct Call {
   int finish() {
     BRM_CUDA(cudaGetLastError());
     for (auto &a : args)
-      if (a.host) BRM_CUDA(cudaMemcpyAsync(a.host, a.dev, a.bytes, cudaMemcpyDeviceToHost, stream));
+      if (a.host) {
+        BRM_CUDA(cudaMemcpyAsync(a.host, a.dev, a.bytes, cudaMemcpyDeviceToHost, stream));
+        count_transfer(0, a.bytes);
+      }
     if (host_out) BRM_CUDA(cudaStreamSynchronize(stream));
     return BRM_OK;
   }
@@ -252,6 +256,7 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   P.path_out = j.path_out;
   P.stop_out = j.stop_out;
   P.vals_offset = smem_model(c);
+  P.steps = step_counter(PK_WALK);
   const int smem = P.vals_offset + 8 * P.chunk;
   if (smem > c->info.max_smem) return fail(BRM_EINVAL, "model image too large for shared memory (%d B)", smem);
   BRM_TRY(call.scratch<double>(2 * (size_t)P.n_items, &P.partials));
@@ -261,7 +266,11 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   if (per_sm < 1) return fail(BRM_EINVAL, "walker does not fit on an SM (smem %d B)", smem);
   const int grid = std::min(P.n_items, per_sm * c->info.sms);
   void *args[] = {&P};
-  BRM_CUDA(cudaLaunchKernel(c->kern.walk, dim3(grid), dim3(kWalkThreads), args, smem, call.stream));
+  {
+    const int tok_ = prof_begin(PK_WALK, call.stream);
+    BRM_CUDA(cudaLaunchKernel(c->kern.walk, dim3(grid), dim3(kWalkThreads), args, smem, call.stream));
+    prof_end(tok_, call.stream);
+  }
   FinishParams F{};
   F.partials = P.partials;
   F.n_units = j.n_units;
@@ -270,13 +279,18 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   F.mode = j.finish_mode;
   F.total_paths = j.total_paths;
   F.points = j.points;
+  F.points_stride = j.start_stride;
   F.d = c->hdr.d;
   F.payoff = c->hdr.payoff;
   F.strike = c->hdr.strike;
   F.out = j.out;
   if (F.out) {
     void *fargs[] = {&F};
+    {
+    const int tok_ = prof_begin(PK_FINISH, call.stream);
     BRM_CUDA(cudaLaunchKernel(finish_kernel(), dim3((j.n_units + 127) / 128), dim3(128), fargs, 0, call.stream));
+    prof_end(tok_, call.stream);
+  }
   }
   return BRM_OK;
 }
@@ -418,6 +432,7 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
   c->info = device_info(device);
   c->kern = kernels_for(d, mode == BRM_MODE_FAST);
   c->blob_bytes = 8 * dbl.size() + 4 * ints.size();
+  count_transfer(c->blob_bytes, 0);
   cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&c->blob, c->blob_bytes);
   if (e == cudaSuccess) e = cudaMemcpy(c->blob, dbl.data(), 8 * dbl.size(), cudaMemcpyHostToDevice);
@@ -485,7 +500,11 @@ int brm_raw_uint64(int32_t device, uint64_t key64, uint64_t stream64, uint64_t s
   BRM_TRY(call.out(out, count, &o));
   const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 16);
   void *args[] = {&key64, &stream64, &start, &count, &o};
-  BRM_CUDA(cudaLaunchKernel(fill_raw_kernel(), dim3(grid), dim3(256), args, 0, call.stream));
+  {
+    const int tok_ = prof_begin(PK_RNG, call.stream);
+    BRM_CUDA(cudaLaunchKernel(fill_raw_kernel(), dim3(grid), dim3(256), args, 0, call.stream));
+    prof_end(tok_, call.stream);
+  }
   BRM_TRY(call.finish());
   BRM_CUDA(cudaStreamSynchronize(call.stream));
   return BRM_OK;
@@ -500,7 +519,11 @@ int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t star
   BRM_TRY(call.out(out, count, &o));
   const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 16);
   void *args[] = {&key64, &stream64, &start, &count, &o};
-  BRM_CUDA(cudaLaunchKernel(fill_normals_kernel(), dim3(grid), dim3(256), args, 0, call.stream));
+  {
+    const int tok_ = prof_begin(PK_RNG, call.stream);
+    BRM_CUDA(cudaLaunchKernel(fill_normals_kernel(), dim3(grid), dim3(256), args, 0, call.stream));
+    prof_end(tok_, call.stream);
+  }
   BRM_TRY(call.finish());
   BRM_CUDA(cudaStreamSynchronize(call.stream));
   return BRM_OK;
@@ -597,7 +620,11 @@ int brm_decisions(brm_ctx *c, const double *states, int64_t n, int32_t m, int32_
   BRM_TRY(allow_smem(c->kern.dec, smem));
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->info.sms * 4);
   void *args[] = {&P};
-  BRM_CUDA(cudaLaunchKernel(c->kern.dec, dim3(grid), dim3(256), args, smem, call.stream));
+  {
+    const int tok_ = prof_begin(PK_DEC, call.stream);
+    BRM_CUDA(cudaLaunchKernel(c->kern.dec, dim3(grid), dim3(256), args, smem, call.stream));
+    prof_end(tok_, call.stream);
+  }
   return call.finish();
 }
 
@@ -690,13 +717,79 @@ int brm_sample_points(brm_ctx *c, int32_t mode, int32_t m, uint64_t seed, int64_
   P.chol = c->blob_dbl(c->hdr.o_chol);
   P.step_mu = c->blob_dbl(c->hdr.o_mu);
   P.step_vol = c->blob_dbl(c->hdr.o_vol);
+  P.payoff = c->hdr.payoff;
+  P.out_stride = c->hdr.d;
   if (mode == 0) {
     BRM_TRY(call.in(bridge, 4 * (size_t)c->hdr.d + 1, &P.bridge));
     if (!P.bridge) return fail(BRM_EINVAL, "bridge scalars are NULL");
   }
   BRM_TRY(call.out(out_points, (size_t)n * c->hdr.d, &P.out));
   void *args[] = {&P};
-  BRM_CUDA(cudaLaunchKernel(sample_kernel(), dim3((unsigned)((n + 127) / 128)), dim3(128), args, 0, call.stream));
+  {
+    const int tok_ = prof_begin(PK_SAMPLE, call.stream);
+    BRM_CUDA(cudaLaunchKernel(sample_kernel(), dim3((unsigned)((n + 127) / 128)), dim3(128), args, 0, call.stream));
+    prof_end(tok_, call.stream);
+  }
+  return call.finish();
+}
+
+int brm_cmc_calc(brm_ctx *c, int32_t sampler, int32_t m, uint64_t seed, int64_t item_lo, int64_t n,
+                 int32_t n_label, const double *bridge, double *out_features, double *out_beta) {
+  if (!c || !out_features || !out_beta) return fail(BRM_EINVAL, "NULL argument");
+  BRM_TRY(check_remaining(c, m));
+  if (m < 1) return fail(BRM_EINVAL, "date index %d outside 1..%d", m, c->hdr.n_dates);
+  if (sampler != 0 && sampler != 1) return fail(BRM_EINVAL, "unknown sampler %d", sampler);
+  if (n_label < 1) return fail(BRM_EINVAL, "need at least one labeling path");
+  if (n < 0 || n > (1 << 26)) return fail(BRM_EINVAL, "point count out of range");
+  if (n == 0) return BRM_OK;
+  DeviceScope scope(c->device);
+  Call call(c->stream());
+  const int d = c->hdr.d, F = d > 1 ? d + 1 : 1;
+  SampleParams S{};
+  S.mode = sampler;
+  S.m = m;
+  S.d = d;
+  S.n_dates = c->hdr.n_dates;
+  S.payoff = c->hdr.payoff;
+  S.out_stride = F;
+  S.seed = seed;
+  S.item_lo = item_lo;
+  S.n = n;
+  S.s0 = c->blob_dbl(c->hdr.o_s0);
+  S.chol = c->blob_dbl(c->hdr.o_chol);
+  S.step_mu = c->blob_dbl(c->hdr.o_mu);
+  S.step_vol = c->blob_dbl(c->hdr.o_vol);
+  if (sampler == 0) {
+    BRM_TRY(call.in(bridge, 4 * (size_t)d + 1, &S.bridge));
+    if (!S.bridge) return fail(BRM_EINVAL, "bridge scalars are NULL");
+  }
+  BRM_TRY(call.out(out_features, (size_t)n * F, &S.out));
+  double *o;
+  BRM_TRY(call.out(out_beta, n, &o));
+  void *sargs[] = {&S};
+  {
+    const int tok_ = prof_begin(PK_SAMPLE, call.stream);
+    BRM_CUDA(cudaLaunchKernel(sample_kernel(), dim3((unsigned)((n + 127) / 128)), dim3(128), sargs, 0, call.stream));
+    prof_end(tok_, call.stream);
+  }
+  WalkJob j;
+  j.n_units = (int)n;
+  j.per_unit = n_label;
+  j.total_paths = n * (int64_t)n_label;
+  j.chunk = std::min(n_label, kMaxChunk);
+  j.m_start = m;
+  j.starts = S.out;
+  j.start_stride = F;
+  j.seed = seed;
+  j.phase = BRM_PHASE_CMC_CALC;
+  j.item_base = item_lo;
+  j.key_date = m;
+  // labels continue the point's stream after the sampler's draws
+  j.draw_base = sampler == 0 ? 2 * (uint64_t)d : (uint64_t)m * d;
+  j.finish_mode = 2;
+  j.points = S.out;
+  j.out = o;
+  BRM_TRY(run_walk(c, call, j));
   return call.finish();
 }
 
@@ -759,6 +852,7 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   while (csize > 1 && (int64_t)csize * kWalkThreads / 2 > n_inner) csize >>= 1;
   const int per_cta = (n_inner + csize - 1) / csize;
   P.vals_offset = smem_model(c);
+  P.steps = step_counter(PK_IZ);
   P.hist_offset = P.vals_offset + ((8 * per_cta + 15) & ~15);
   const int smem = P.hist_offset + 8 * (P.max_iter + 1);
   if (smem > c->info.max_smem) return fail(BRM_EINVAL, "probe solve needs %d B of shared memory", smem);
@@ -776,7 +870,11 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void *args[] = {&P};
-  BRM_CUDA(cudaLaunchKernelExC(&cfg, c->kern.iz, args));
+  {
+    const int tok_ = prof_begin(PK_IZ, call.stream);
+    BRM_CUDA(cudaLaunchKernelExC(&cfg, c->kern.iz, args));
+    prof_end(tok_, call.stream);
+  }
   return call.finish();
 }
 

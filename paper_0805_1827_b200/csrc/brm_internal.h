@@ -1,6 +1,7 @@
 // brm_internal.h -- kernel parameter blocks shared by the kernels and the C ABI.
 #pragma once
 #include <cstdint>
+#include <cuda_runtime.h>
 
 #include "brm_model.cuh"
 
@@ -28,6 +29,7 @@ struct WalkParams {
   uint64_t nrm_base, nrm_count;
   int vals_offset;  // byte offset of the per-path value buffer in dynamic smem
   double *partials;  // [n_items][2]
+  unsigned long long *steps;  // executed path-steps counter (may be null)
   double *path_out;  // optional [n_units * per_unit]
   int32_t *stop_out;
 };
@@ -37,6 +39,7 @@ struct FinishParams {
   int n_units, chunks_per_unit, per_unit, mode;
   int64_t total_paths;
   const double *points;  // mode 2
+  int points_stride;
   int d, payoff;
   double strike;
   double *out;
@@ -59,6 +62,7 @@ struct IzParams {
   const double *normals;
   uint64_t nrm_base, nrm_count;
   int vals_offset, hist_offset;
+  unsigned long long *steps;
   double *out_level;
   int32_t *out_iter, *out_conv;
 };
@@ -73,7 +77,8 @@ struct DecisionParams {
 };
 
 struct SampleParams {
-  int mode, m, d, n_dates;
+  int mode, m, d, n_dates, payoff;
+  int out_stride;  // d, or d+1 with the derived classifier feature in column d
   uint64_t seed;
   int64_t item_lo, n;
   const double *s0, *chol, *step_mu, *step_vol, *bridge;
@@ -83,6 +88,14 @@ struct SampleParams {
 struct KernelTriple {
   void *walk, *iz, *dec;
 };
+
+// Kernel families for launch accounting (brm_prof.cu, BRM_PROF_* in the C ABI).
+enum ProfKind { PK_WALK = 0, PK_IZ = 1, PK_BOOST = 2, PK_SAMPLE = 3, PK_FINISH = 4, PK_LSTSQ = 5, PK_RNG = 6,
+                PK_DEC = 7, PK_AUX = 8, kProfKinds = 9 };
+int prof_begin(int kind, cudaStream_t s);
+void prof_end(int token, cudaStream_t s);
+unsigned long long *step_counter(int kind);
+void count_transfer(size_t h2d, size_t d2h);
 
 KernelTriple kernels_for(int d, bool fast);
 int set_error(int code, const char *fmt, ...);

@@ -27,7 +27,7 @@ __global__ void finish_units(FinishParams P) {
     M.d = P.d;
     M.payoff = P.payoff;
     M.strike = P.strike;
-    const double *x = P.points + (size_t)u * P.d;
+    const double *x = P.points + (size_t)u * P.points_stride;
     P.out[u] = __dsub_rn(payoff<0>(M, x), __ddiv_rn(s, (double)P.per_unit));
   }
 }
@@ -37,13 +37,22 @@ __global__ void finish_units(FinishParams P) {
 // bridge to t_m (draws d..2d-1) exactly as boundary_cmc.py:164-177 with
 // market.py:180-220 (z @ L^T summed over a in order); mode 1: forward steps
 // over dates 1..m with the walker's step and parity draws k*d + a.
+// Derived classifier feature x[d] (boundary_cmc.py:38-52 for the max-call).
+__device__ inline void write_aggregate(const SampleParams &P, double *x) {
+  if (P.out_stride <= P.d) return;
+  Model<double> M{};
+  M.d = P.d;
+  M.payoff = P.payoff;
+  x[P.d] = aggregate<0>(M, x);
+}
+
 __global__ void sample_points(SampleParams P) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= P.n) return;
   const int d = P.d;
   uint64_t key, stream;
   derive_words(P.seed, 2 /* CMC_CALC */, (uint64_t)(P.item_lo + i), (uint64_t)P.m, key, stream);
-  double *x = P.out + i * d;
+  double *x = P.out + i * P.out_stride;
   const double *L = P.chol;
   if (P.mode == 1) {
     double v[kMaxD], z[kMaxD];
@@ -58,6 +67,7 @@ __global__ void sample_points(SampleParams P) {
       }
     }
     for (int a = 0; a < d; ++a) x[a] = v[a];
+    write_aggregate(P, x);
     return;
   }
   const double *drift_T = P.bridge, *sig_sqrt_T = P.bridge + d, *log_s0 = P.bridge + 2 * d;
@@ -72,6 +82,7 @@ __global__ void sample_points(SampleParams P) {
   }
   if (P.m == P.n_dates) {
     for (int r = 0; r < d; ++r) x[r] = term[r];
+    write_aggregate(P, x);
     return;
   }
   const double one_m_lam = __dsub_rn(1.0, lam);
@@ -83,6 +94,7 @@ __global__ void sample_points(SampleParams P) {
                                 __dmul_rn(bsd[r], y));
     x[r] = exp(lm);
   }
+  write_aggregate(P, x);
 }
 
 // ------------------------------------------------------------------ RNG ----

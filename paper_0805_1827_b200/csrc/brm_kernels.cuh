@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kWalkThreads) walk_units(WalkParams P) {
       double *pout = P.path_out ? P.path_out + (size_t)u * P.per_unit : nullptr;
       int32_t *sout = P.stop_out ? P.stop_out + (size_t)u * P.per_unit : nullptr;
       walk_paths<D, FAST>(M, s_start, P.m_start, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, pout,
-                          sout);
+                          sout, P.steps);
     }
     __syncthreads();
     double s = 0.0, q = 0.0;
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kWalkThreads) iz_probes(IzParams P) {
     const uint64_t base0 = unit_base<FAST>(draw_base, P.normals != nullptr);
     if (p0 < p1)
       walk_paths<D, FAST>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, nullptr,
-                          nullptr);
+                          nullptr, P.steps);
     __syncthreads();
     double s = 0.0, q = 0.0;
     fold_values(vals, p1 > p0 ? p1 - p0 : 0, s_red, s, q);

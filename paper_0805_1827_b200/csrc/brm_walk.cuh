@@ -66,7 +66,8 @@ __host__ __device__ __forceinline__ uint64_t unit_base(uint64_t draw_base, bool 
 template <int D, bool FAST>
 __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_start, int m_start, int n_steps,
                            uint64_t key, uint64_t stream, uint64_t base0, int p0, int p1, const NormalSrc &ns,
-                           double *vals, int *s_next, double *path_out, int32_t *stop_out) {
+                           double *vals, int *s_next, double *path_out, int32_t *stop_out,
+                           unsigned long long *step_count) {
   using R = RealT<FAST>;
   const int d = dim_of<D>(M.d);
   const uint64_t stride = path_stride<FAST>(d, n_steps, ns.ptr != nullptr);
@@ -75,6 +76,7 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
   constexpr int NV = D > 0 ? D : kMaxD;
   R v[NV], z[NV];
 
+  unsigned nsteps = 0;
   int p = p0 + threadIdx.x;
   bool have = p < p1;
   int k = 0;
@@ -87,6 +89,7 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
     double val = 0.0;
     int stop_m = 0;
     if (have) {
+      ++nsteps;
       path_step_draws<D, FAST>(d, key, stream, base, k, ns, z);
       gbm_step<D>(M, v, z);
       const int m = m_start + k + 1;
@@ -121,6 +124,11 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
         for (int i = 0; i < dim_of<D>(d); ++i) v[i] = s_start[i];
       }
     }
+  }
+  if (step_count) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) nsteps += __shfl_down_sync(0xffffffffu, nsteps, off);
+    if (lane == 0 && nsteps) atomicAdd(step_count, (unsigned long long)nsteps);
   }
 }
 

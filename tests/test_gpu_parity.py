@@ -198,7 +198,7 @@ def test_fit_ensemble_vs_oracle(n, F, rounds, seed):
     X = 100 * np.exp(0.2 * rng.normal(size=(n, F)))
     X[:, -1] = X.max(axis=1) if F > 1 else X[:, -1]
     beta = (X[:, 0] - 100) + 0.5 * (X[:, -1] - 110) + 5 * rng.normal(size=n)
-    gf, gt, gp, ga, gi = G.fit_ensemble_arrays(X, beta, rounds, mode="parity")
+    gf, gt, gp, ga, _, gi = G.fit_ensemble_arrays(X, beta, rounds, mode="parity")
     of, ot, op, oa, oi = O.fit_ensemble(X, beta, rounds)
     assert len(gf) == len(of) and gi == oi
     assert np.array_equal(gf, of) and np.array_equal(gt, ot) and np.array_equal(gp, op)
@@ -207,10 +207,10 @@ def test_fit_ensemble_vs_oracle(n, F, rounds, seed):
 
 def test_fit_ensemble_one_class_and_constant():
     X = np.ones((50, 3))
-    f, t, p, a, i = G.fit_ensemble_arrays(X, np.ones(50), 5)
+    f, t, p, a, _, i = G.fit_ensemble_arrays(X, np.ones(50), 5)
     assert len(f) == 0 and i == 1.0
     beta = np.where(np.arange(50) < 20, 1.0, -1.0)
-    f, t, p, a, i = G.fit_ensemble_arrays(X, beta, 5)
+    f, t, p, a, _, i = G.fit_ensemble_arrays(X, beta, 5)
     of, ot, op, oa, oi = O.fit_ensemble(X, beta, 5)
     assert list(f) == of and list(p) == op and np.allclose(a, oa, rtol=1e-12) and i == oi
 
