@@ -18,9 +18,11 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -57,54 +59,6 @@ __device__ double pw_leaf(const double *a, int n) {
   return res;
 }
 
-// Leaves of numpy's recursion over n elements, left to right (host side).
-static void pw_leaves(int64_t off, int64_t n, std::vector<int2> &out) {
-  if (n <= kPwBlock) {
-    out.push_back(make_int2((int)off, (int)n));
-    return;
-  }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  pw_leaves(off, n2, out);
-  pw_leaves(off + n2, n - n2, out);
-}
-
-// Combine leaf sums along the same recursion (thread-local, iterative).
-__device__ double pw_combine(const double *leaf, int n) {
-  // explicit stack of (len, state); a node of len <= 128 consumes one leaf
-  struct Frame {
-    int len;
-    int stage;
-    double left;
-  };
-  Frame st[48];
-  int sp = 0, next_leaf = 0;
-  double ret = 0.0;
-  st[sp++] = Frame{n, 0, 0.0};
-  while (sp > 0) {
-    Frame &f = st[sp - 1];
-    if (f.len <= kPwBlock) {
-      ret = leaf[next_leaf++];
-      --sp;
-      continue;
-    }
-    int n2 = f.len / 2;
-    n2 -= n2 % 8;
-    if (f.stage == 0) {
-      f.stage = 1;
-      st[sp++] = Frame{n2, 0, 0.0};
-    } else if (f.stage == 1) {
-      f.left = ret;
-      f.stage = 2;
-      st[sp++] = Frame{f.len - n2, 0, 0.0};
-    } else {
-      ret = __dadd_rn(f.left, ret);
-      --sp;
-    }
-  }
-  return ret;
-}
-
 // numpy pairwise sum of a[0..n) by one thread (rare paths only).
 __device__ double pw_serial(const double *a, int n) {
   struct Frame {
@@ -139,36 +93,101 @@ __device__ double pw_serial(const double *a, int n) {
   return ret;
 }
 
-// CTA-wide numpy-order sum of a[0..n); result broadcast to all threads.
-__device__ double cta_pairwise(const double *a, int n, const int2 *leaves, int n_leaves, double *s_leaf,
-                               double *s_out) {
-  for (int l = threadIdx.x; l < n_leaves; l += blockDim.x) s_leaf[l] = pw_leaf(a + leaves[l].x, leaves[l].y);
-  __syncthreads();
-  if (threadIdx.x == 0) *s_out = n == 0 ? 0.0 : pw_combine(s_leaf, n);
-  __syncthreads();
-  const double r = *s_out;
-  __syncthreads();
-  return r;
+// numpy's pairwise recursion over n elements as a tree: leaves in order,
+// internal nodes grouped by height so a CTA combines a level at a time.
+struct PwTree {
+  std::vector<int2> leaves;    // (offset, length), left to right
+  std::vector<int2> children;  // internal node L+j = children[j].x + children[j].y
+  std::vector<int> level_end;  // internal nodes [level_end[h-1], level_end[h]) have height h+1
+};
+
+// Build the tree with explicit node ids: leaves 0..L-1, internal nodes L.. in
+// level order.  Returns the root id.
+static int pw_tree(int64_t n, PwTree &t) {
+  struct Node {
+    int left, right, height;
+  };
+  std::vector<Node> inner;
+  std::function<int(int64_t, int64_t)> rec = [&](int64_t off, int64_t len) -> int {
+    if (len <= kPwBlock) {
+      t.leaves.push_back(make_int2((int)off, (int)len));
+      return -(int)t.leaves.size();  // leaf k encoded as -(k+1)
+    }
+    int64_t n2 = len / 2;
+    n2 -= n2 % 8;
+    const int l = rec(off, n2);
+    const int r = rec(off + n2, len - n2);
+    auto h = [&](int id) { return id < 0 ? 0 : inner[id].height; };
+    inner.push_back(Node{l, r, 1 + std::max(h(l), h(r))});
+    return (int)inner.size() - 1;
+  };
+  const int root = rec(0, n);
+  const int L = (int)t.leaves.size();
+  if (root < 0) return 0;
+  // order internal nodes by height
+  std::vector<int> order(inner.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return inner[x].height < inner[y].height; });
+  std::vector<int> newid(inner.size());
+  for (size_t k = 0; k < order.size(); ++k) newid[order[k]] = L + (int)k;
+  auto idof = [&](int id) { return id < 0 ? (-id - 1) : newid[id]; };
+  int maxh = 0;
+  for (size_t k = 0; k < order.size(); ++k) {
+    const Node &nd = inner[order[k]];
+    t.children.push_back(make_int2(idof(nd.left), idof(nd.right)));
+    maxh = std::max(maxh, nd.height);
+  }
+  t.level_end.assign(maxh, 0);
+  for (size_t k = 0; k < order.size(); ++k) t.level_end[inner[order[k]].height - 1] = (int)k + 1;
+  return newid[root];
 }
 
 struct BoostParams {
   int n, F, rounds;
   const double *xs;        // [n][F]
   const double *xsorted;   // [F][n]
-  const int *order;        // [F][n]
   const double *y;         // [n] +-1
-  double *w;               // [n]
-  double *pcum, *ncum;     // [F][n]
+  double *w;               // [n] unnormalised weights of the current round
+  double *wn;              // [F][n] per-CTA normalised copy (w / sum(w), numpy order)
+  const int *pos_idx;      // [F][n] sample ids of the positives in sorted order (first n_pos[f])
+  const int *neg_idx;      // [F][n] sample ids of the negatives in sorted order
+  const int *cntpos;       // [F][n] positives among sorted positions 0..i
+  double *pcum, *ncum;     // [F][n] prefix sums of the positive / negative chains
   const int2 *leaves;
   int n_leaves;
+  const int2 *children;
+  const int *level_end;
+  int n_levels, root;
   double *feat_err;        // [F]
   int *feat_pos;           // [F] 2*i + (pol == -1)
   double *wsub;            // [F][n] per-CTA scratch for the constant-stump sums
   int *out_feat;
   double *out_thr, *out_pol, *out_alpha, *out_err;
   int *out_count;
+  int n_pos;
   int raw;  // 1: one fit_stump search with the given weights, no boosting rules
 };
+
+// CTA-wide numpy-order sum of a[0..n) (a divided by `div` on the fly when
+// div != 1); every thread gets the result.  s_node holds L + I doubles.
+__device__ double cta_pairwise(const BoostParams &P, const double *a, double *s_node) {
+  const int L = P.n_leaves;
+  for (int l = threadIdx.x; l < L; l += blockDim.x) s_node[l] = pw_leaf(a + P.leaves[l].x, P.leaves[l].y);
+  __syncthreads();
+  int lo = 0;
+  for (int h = 0; h < P.n_levels; ++h) {
+    const int hi = P.level_end[h];
+    for (int j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+      const int2 c = P.children[j];
+      s_node[L + j] = __dadd_rn(s_node[c.x], s_node[c.y]);
+    }
+    lo = hi;
+    __syncthreads();
+  }
+  const double r = s_node[P.root];
+  __syncthreads();
+  return r;
+}
 
 struct Cand {
   double err;
@@ -179,73 +198,96 @@ __device__ __forceinline__ bool cand_less(const Cand &a, const Cand &b) {
   return a.err < b.err || (a.err == b.err && a.key < b.key);
 }
 
+// Sequential prefix sums out[k] = in[0] + ... + in[k] continuing from *acc
+// (one thread).  Loads are batched ahead of the dependent adds.
+__device__ __forceinline__ void serial_chain(const double *__restrict__ in, double *__restrict__ out, int cnt,
+                                             double &acc) {
+  constexpr int B = 8;
+  int k = 0;
+  double cur[B];
+  if (cnt >= B) {
+#pragma unroll
+    for (int j = 0; j < B; ++j) cur[j] = in[j];
+  }
+  for (; k + B <= cnt; k += B) {
+    double nxt[B];
+    const bool more = k + 2 * B <= cnt;
+#pragma unroll
+    for (int j = 0; j < B; ++j) nxt[j] = more ? in[k + B + j] : 0.0;
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      acc = __dadd_rn(acc, cur[j]);
+      out[k + j] = acc;
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) cur[j] = nxt[j];
+  }
+  for (; k < cnt; ++k) {
+    acc = __dadd_rn(acc, in[k]);
+    out[k] = acc;
+  }
+}
+
 __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double *s_leaf = reinterpret_cast<double *>(smem_raw);        // [n_leaves]
-  double *s_w = s_leaf + P.n_leaves;                            // [kTile] sorted weights
-  double *s_pc = s_w + kTile;                                   // [kTile]
-  double *s_nc = s_pc + kTile;                                  // [kTile]
-  unsigned char *s_pos = reinterpret_cast<unsigned char *>(s_nc + kTile);  // [kTile]
-  __shared__ double s_sum;
+  double *s_node = reinterpret_cast<double *>(smem_raw);               // [L + I]
+  double *s_in_p = s_node + 2 * P.n_leaves;                            // [kTile]
+  double *s_in_n = s_in_p + kTile;                                     // [kTile]
+  double *s_out_p = s_in_n + kTile;                                    // [kTile]
+  double *s_out_n = s_out_p + kTile;                                   // [kTile]
   __shared__ Cand s_cand[kBoostThreads / 32];
   __shared__ int s_stop;
-  __shared__ double s_alpha, s_thr, s_pol;
+  __shared__ double s_alpha, s_thr, s_pol, s_err;
   __shared__ int s_feat;
 
   const int n = P.n, F = P.F;
   const int f = blockIdx.x;
   const int slice = (n + gridDim.x - 1) / gridDim.x;
   const int w_lo = blockIdx.x * slice, w_hi = min(w_lo + slice, n);
+  double *wn = P.wn + (size_t)f * n;
   int count = 0;
 
   for (int round = 0; round < P.rounds; ++round) {
+    // ---- w / w.sum() (numpy pairwise order), CTA-private copy ------------
+    const double s = round == 0 ? 1.0 : cta_pairwise(P, P.w, s_node);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) wn[i] = round == 0 ? P.w[i] : __ddiv_rn(P.w[i], s);
+    __syncthreads();
+    const double total = cta_pairwise(P, wn, s_node);
     // ---- split search on feature f -------------------------------------
-    const double total = cta_pairwise(P.w, n, P.leaves, P.n_leaves, s_leaf, &s_sum);
     if (f < F) {
-      const int *ord = P.order + (size_t)f * n;
+      const int *pid = P.pos_idx + (size_t)f * n;
+      const int *nid = P.neg_idx + (size_t)f * n;
       double *pc = P.pcum + (size_t)f * n;
       double *nc = P.ncum + (size_t)f * n;
-      double pacc = 0.0, nacc = 0.0;
-      for (int t0 = 0; t0 < n; t0 += kTile) {
-        const int tn = min(kTile, n - t0);
-        for (int j = threadIdx.x; j < tn; j += blockDim.x) {
-          const int idx = ord[t0 + j];
-          s_w[j] = P.w[idx];
-          s_pos[j] = P.y[idx] > 0.0;
-        }
+      const int n_pos = P.n_pos, n_neg = n - P.n_pos;
+      double pacc = 0.0, nacc = 0.0;  // np.cumsum(where(y>0, w, 0)): zeros never change a partial sum
+      for (int t0 = 0; t0 < max(n_pos, n_neg); t0 += kTile) {
+        const int tp = max(0, min(kTile, n_pos - t0)), tn = max(0, min(kTile, n_neg - t0));
+        for (int j = threadIdx.x; j < tp; j += blockDim.x) s_in_p[j] = wn[pid[t0 + j]];
+        for (int j = threadIdx.x; j < tn; j += blockDim.x) s_in_n[j] = wn[nid[t0 + j]];
         __syncthreads();
-        // np.cumsum(where(y>0, w, 0)): adding 0.0 never changes a partial sum,
-        // so the positive and negative prefix chains run independently.
-        if (threadIdx.x == 0) {
-          for (int j = 0; j < tn; ++j) {
-            if (s_pos[j]) pacc = __dadd_rn(pacc, s_w[j]);
-            s_pc[j] = pacc;
-          }
-        } else if (threadIdx.x == 32) {
-          for (int j = 0; j < tn; ++j) {
-            if (!s_pos[j]) nacc = __dadd_rn(nacc, s_w[j]);
-            s_nc[j] = nacc;
-          }
-        }
+        if (threadIdx.x == 0) serial_chain(s_in_p, s_out_p, tp, pacc);
+        else if (threadIdx.x == 32) serial_chain(s_in_n, s_out_n, tn, nacc);
         __syncthreads();
-        for (int j = threadIdx.x; j < tn; j += blockDim.x) {
-          pc[t0 + j] = s_pc[j];
-          nc[t0 + j] = s_nc[j];
-        }
-        __syncthreads();
+        for (int j = threadIdx.x; j < tp; j += blockDim.x) pc[t0 + j] = s_out_p[j];
+        for (int j = threadIdx.x; j < tn; j += blockDim.x) nc[t0 + j] = s_out_n[j];
       }
-      __threadfence_block();
+      __syncthreads();
       const double *xf = P.xsorted + (size_t)f * n;
-      const double tot_neg = nc[n - 1];
+      const int *cp = P.cntpos + (size_t)f * n;
+      const double tot_neg = n_neg > 0 ? nc[n_neg - 1] : 0.0;
       Cand best{__longlong_as_double(0x7ff0000000000000LL), 0x7fffffff};
       for (int i = threadIdx.x; i < n - 1; i += blockDim.x) {
         if (!(__dsub_rn(xf[i + 1], xf[i]) > 0.0)) continue;
-        const double ep = __dadd_rn(pc[i], __dsub_rn(tot_neg, nc[i]));
+        const int np_ = cp[i], nn_ = i + 1 - np_;
+        const double pcs = np_ > 0 ? pc[np_ - 1] : 0.0;
+        const double ncs = nn_ > 0 ? nc[nn_ - 1] : 0.0;
+        const double ep = __dadd_rn(pcs, __dsub_rn(tot_neg, ncs));
         const double em = __dsub_rn(total, ep);
-        const Cand a{ep, 2 * i}, b{em, 2 * i + 1};
-        if (cand_less(a, best)) best = a;
-        if (cand_less(b, best)) best = b;
+        const Cand ca{ep, 2 * i}, cb{em, 2 * i + 1};
+        if (cand_less(ca, best)) best = ca;
+        if (cand_less(cb, best)) best = cb;
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
@@ -274,54 +316,43 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
           bf = g;
           bk = P.feat_pos[g];
         }
-      double thr, pol, err;
-      int feat;
       if (bf < 0) {
-        // every feature constant: weighted majority constant stump
-        feat = 0;
-        thr = __longlong_as_double(0xfff0000000000000LL);
-        s_stop = 2;  // resolved below by the whole CTA
-        pol = 0.0;
-        err = 0.0;
+        s_stop = 2;  // every feature constant: resolved below by the whole CTA
+        s_feat = 0;
+        s_thr = __longlong_as_double(0xfff0000000000000LL);
       } else {
-        feat = bf;
         const int i = bk >> 1;
         const double *xf = P.xsorted + (size_t)bf * n;
-        thr = __dmul_rn(0.5, __dadd_rn(xf[i], xf[i + 1]));
-        pol = (bk & 1) ? -1.0 : 1.0;
-        err = be;
+        s_feat = bf;
+        s_thr = __dmul_rn(0.5, __dadd_rn(xf[i], xf[i + 1]));
+        s_pol = (bk & 1) ? -1.0 : 1.0;
+        s_err = be;
         s_stop = 0;
       }
-      s_feat = feat;
-      s_thr = thr;
-      s_pol = pol;
-      s_alpha = err;  // holds err until alpha is formed
     }
     __syncthreads();
     if (s_stop == 2) {
       // every feature constant (boosting.py:166-170): pol = +1 iff sum(w*y) >= 0,
-      // err = sum(w[y != pol]), both in numpy's pairwise order; per-CTA scratch
+      // err = sum(w[y != pol]), both in numpy's pairwise order
       double *ws = P.wsub + (size_t)blockIdx.x * n;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) ws[i] = __dmul_rn(P.w[i], P.y[i]);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) ws[i] = __dmul_rn(wn[i], P.y[i]);
       __syncthreads();
-      const double swy = cta_pairwise(ws, n, P.leaves, P.n_leaves, s_leaf, &s_sum);
+      const double swy = cta_pairwise(P, ws, s_node);
       const double pol = swy >= 0.0 ? 1.0 : -1.0;
       if (threadIdx.x == 0) {
         int k = 0;
         for (int i = 0; i < n; ++i)
-          if (P.y[i] != pol) ws[k++] = P.w[i];
-        s_feat = 0;
+          if (P.y[i] != pol) ws[k++] = wn[i];
         s_pol = pol;
-        s_alpha = pw_serial(ws, k);
+        s_err = pw_serial(ws, k);
         s_stop = 0;
       }
       __syncthreads();
     }
     // alpha = 0.5 * log((1 - err) / max(err, 1e-10)); stop rules of fit_ensemble
     if (threadIdx.x == 0) {
-      const double err = s_alpha;
+      const double err = s_err;
       if (P.raw) {
-        // fit_stump semantics (boosting.py:126-171): best stump and its error only
         if (blockIdx.x == 0) {
           P.out_feat[0] = s_feat;
           P.out_thr[0] = s_thr;
@@ -349,24 +380,49 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
     if (s_stop == 1) break;
     ++count;
     if (s_stop == 3 || round + 1 == P.rounds) break;
-    // ---- reweight: w *= exp(-alpha * y * pred); then w /= sum(w) -----------
+    // ---- reweight own slice: w = (w / sum) * exp(-alpha * y * pred) ------
     {
       const double a = s_alpha, thr = s_thr, pol = s_pol;
       const int feat = s_feat;
       const double e_agree = exp(-a), e_miss = exp(a);
       for (int i = w_lo + threadIdx.x; i < w_hi; i += blockDim.x) {
         const double pred = P.xs[(size_t)i * F + feat] > thr ? pol : -pol;
-        P.w[i] = __dmul_rn(P.w[i], (P.y[i] * pred > 0.0) ? e_agree : e_miss);
+        P.w[i] = __dmul_rn(wn[i], (P.y[i] * pred > 0.0) ? e_agree : e_miss);
       }
-    }
-    grid.sync();
-    {
-      const double s = cta_pairwise(P.w, n, P.leaves, P.n_leaves, s_leaf, &s_sum);
-      for (int i = w_lo + threadIdx.x; i < w_hi; i += blockDim.x) P.w[i] = __ddiv_rn(P.w[i], s);
     }
     grid.sync();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *P.out_count = count;
+}
+
+// Per feature: ids of positives / negatives in sorted order and the running
+// count of positives (once per fit; labels and order are fixed across rounds).
+__global__ void __launch_bounds__(256) split_classes(const int *order, const double *y, int n, int *pos_idx,
+                                                     int *neg_idx, int *cntpos) {
+  using Scan = cub::BlockScan<int, 256>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_carry;
+  const int f = blockIdx.x;
+  const int *ord = order + (size_t)f * n;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int t0 = 0; t0 < n; t0 += 256) {
+    const int i = t0 + threadIdx.x;
+    const int id = i < n ? ord[i] : 0;
+    const int pos = (i < n && y[id] > 0.0) ? 1 : 0;
+    int excl, tile_total;
+    Scan(tmp).ExclusiveSum(pos, excl, tile_total);
+    const int carry = s_carry;
+    if (i < n) {
+      const int before = carry + excl;  // positives strictly before position i
+      cntpos[(size_t)f * n + i] = before + pos;
+      if (pos) pos_idx[(size_t)f * n + before] = id;
+      else neg_idx[(size_t)f * n + (i - before)] = id;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = carry + tile_total;
+    __syncthreads();
+  }
 }
 
 __global__ void transpose_cols(const double *xs, int n, int F, double *xt, int *iota) {
@@ -515,6 +571,26 @@ bool is_dev(const void *p) {
     }                                                                                    \
   } while (0)
 
+namespace {
+// Stream-ordered scratch that frees itself.
+struct Scratch {
+  cudaStream_t s;
+  std::vector<void *> ptrs;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  ~Scratch() {
+    for (void *p : ptrs) cudaFreeAsync(p, s);
+  }
+  template <typename T>
+  cudaError_t get(T **p, size_t count) {
+    void *q = nullptr;
+    cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(count, 1) * sizeof(T), s);
+    if (e == cudaSuccess) ptrs.push_back(q);
+    *p = static_cast<T *>(q);
+    return e;
+  }
+};
+}  // namespace
+
 extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, void *stream, const double *xs,
                                 const double *betas, const double *weights, int64_t n64, int32_t F, int32_t rounds,
                                 int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha,
@@ -533,130 +609,153 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  double *d_xs = nullptr, *d_b = nullptr, *d_xt = nullptr, *d_xsorted = nullptr, *d_y = nullptr, *d_w = nullptr;
-  double *d_pc = nullptr, *d_nc = nullptr, *d_err = nullptr, *d_wsub = nullptr, *d_thr = nullptr, *d_pol = nullptr,
-         *d_alpha = nullptr, *d_rerr = nullptr;
-  int *d_iota = nullptr, *d_order = nullptr, *d_pos = nullptr, *d_npos = nullptr, *d_feat = nullptr,
-      *d_count = nullptr;
-  int2 *d_leaves = nullptr;
-  void *d_tmp = nullptr;
-  size_t tmp_bytes = 0;
-  int npos = 0;
-  std::vector<int2> leaves;
-  BCU(cudaMallocAsync(&d_xs, sizeof(double) * (size_t)n * F, s));
-  BCU(cudaMemcpyAsync(d_xs, xs, sizeof(double) * (size_t)n * F, cudaMemcpyDefault, s));
-  if (!is_dev(xs)) count_transfer(sizeof(double) * (size_t)n * F, 0);
-  if (!is_dev(betas)) count_transfer(sizeof(double) * n, 0);
-  BCU(cudaMallocAsync(&d_b, sizeof(double) * n, s));
-  BCU(cudaMemcpyAsync(d_b, betas, sizeof(double) * n, cudaMemcpyDefault, s));
-  BCU(cudaMallocAsync(&d_y, sizeof(double) * n, s));
-  BCU(cudaMallocAsync(&d_npos, sizeof(int), s));
-  BCU(cudaMemsetAsync(d_npos, 0, sizeof(int), s));
   {
-    const int tok = prof_begin(PK_AUX, s);
-    labels_from_betas<<<(n + 255) / 256, 256, 0, s>>>(d_b, n, d_y, d_npos);
-    prof_end(tok, s);
-  }
-  BCU(cudaMemcpyAsync(&npos, d_npos, sizeof(int), cudaMemcpyDeviceToHost, s));
-  BCU(cudaStreamSynchronize(s));
-  if (!raw && (npos == 0 || npos == n)) {
-    // one class: zero-round ensemble carrying the class sign (boosting.py:185-187)
-    *out_count = 0;
-    *out_intercept = npos == n ? 1.0 : -1.0;
-    goto done;
-  }
-  BCU(cudaMallocAsync(&d_xt, sizeof(double) * (size_t)n * F, s));
-  BCU(cudaMallocAsync(&d_xsorted, sizeof(double) * (size_t)n * F, s));
-  BCU(cudaMallocAsync(&d_iota, sizeof(int) * n, s));
-  BCU(cudaMallocAsync(&d_order, sizeof(int) * (size_t)n * F, s));
-  {
-    const int tok = prof_begin(PK_AUX, s);
-    transpose_cols<<<(unsigned)(((int64_t)n * F + 255) / 256), 256, 0, s>>>(d_xs, n, F, d_xt, d_iota);
-    prof_end(tok, s);
-  }
-  BCU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_xt, d_xsorted, d_iota, d_order, n, 0, 64, s));
-  BCU(cudaMallocAsync(&d_tmp, tmp_bytes, s));
-  for (int f = 0; f < F; ++f)
-    BCU(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_xt + (size_t)f * n, d_xsorted + (size_t)f * n, d_iota,
-                                        d_order + (size_t)f * n, n, 0, 64, s));
-  BCU(cudaMallocAsync(&d_w, sizeof(double) * n, s));
-  if (weights) {
-    BCU(cudaMemcpyAsync(d_w, weights, sizeof(double) * n, cudaMemcpyDefault, s));
-  } else {
-    const int tok = prof_begin(PK_AUX, s);
-    fill_value<<<(n + 255) / 256, 256, 0, s>>>(d_w, n, 1.0 / n);
-    prof_end(tok, s);
-  }
-  BCU(cudaMallocAsync(&d_pc, sizeof(double) * (size_t)n * F, s));
-  BCU(cudaMallocAsync(&d_nc, sizeof(double) * (size_t)n * F, s));
-  BCU(cudaMallocAsync(&d_err, sizeof(double) * F, s));
-  BCU(cudaMallocAsync(&d_pos, sizeof(int) * F, s));
-  BCU(cudaMallocAsync(&d_wsub, sizeof(double) * (size_t)n * F, s));
-  BCU(cudaMallocAsync(&d_feat, sizeof(int) * rounds, s));
-  BCU(cudaMallocAsync(&d_thr, sizeof(double) * rounds, s));
-  BCU(cudaMallocAsync(&d_pol, sizeof(double) * rounds, s));
-  BCU(cudaMallocAsync(&d_alpha, sizeof(double) * rounds, s));
-  BCU(cudaMallocAsync(&d_rerr, sizeof(double) * rounds, s));
-  BCU(cudaMallocAsync(&d_count, sizeof(int), s));
-  pw_leaves(0, n, leaves);
-  BCU(cudaMallocAsync(&d_leaves, sizeof(int2) * leaves.size(), s));
-  BCU(cudaMemcpyAsync(d_leaves, leaves.data(), sizeof(int2) * leaves.size(), cudaMemcpyHostToDevice, s));
-  {
-    BoostParams P{};
-    P.n = n;
-    P.F = F;
-    P.rounds = rounds;
-    P.raw = raw ? 1 : 0;
-    P.xs = d_xs;
-    P.xsorted = d_xsorted;
-    P.order = d_order;
-    P.y = d_y;
-    P.w = d_w;
-    P.pcum = d_pc;
-    P.ncum = d_nc;
-    P.leaves = d_leaves;
-    P.n_leaves = (int)leaves.size();
-    P.feat_err = d_err;
-    P.feat_pos = d_pos;
-    P.wsub = d_wsub;
-    P.out_feat = d_feat;
-    P.out_thr = d_thr;
-    P.out_pol = d_pol;
-    P.out_alpha = d_alpha;
-    P.out_err = d_rerr;
-    P.out_count = d_count;
-    const size_t smem = sizeof(double) * (leaves.size() + 3 * kTile) + kTile;
-    BCU(cudaFuncSetAttribute(boost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    void *args[] = {&P};
-    const int tok = prof_begin(PK_BOOST, s);
-    BCU(cudaLaunchCooperativeKernel((void *)boost_kernel, dim3(F), dim3(kBoostThreads), args, smem, s));
-    prof_end(tok, s);
-  }
-  BCU(cudaGetLastError());
-  {
-    int count = 0;
-    BCU(cudaMemcpyAsync(&count, d_count, sizeof(int), cudaMemcpyDeviceToHost, s));
+    Scratch S(s);
+    double *d_xs, *d_b, *d_xt, *d_xsorted, *d_y, *d_w, *d_wn, *d_pc, *d_nc, *d_err, *d_wsub, *d_thr, *d_pol,
+        *d_alpha, *d_rerr;
+    int *d_iota, *d_order, *d_pos, *d_npos, *d_feat, *d_count, *d_pid, *d_nid, *d_cnt, *d_lvl;
+    int2 *d_leaves, *d_children;
+    void *d_tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int npos = 0;
+    PwTree tree;
+    int root = 0;
+    BCU(S.get(&d_xs, (size_t)n * F));
+    BCU(cudaMemcpyAsync(d_xs, xs, sizeof(double) * (size_t)n * F, cudaMemcpyDefault, s));
+    if (!is_dev(xs)) count_transfer(sizeof(double) * (size_t)n * F, 0);
+    if (!is_dev(betas)) count_transfer(sizeof(double) * n, 0);
+    BCU(S.get(&d_b, n));
+    BCU(cudaMemcpyAsync(d_b, betas, sizeof(double) * n, cudaMemcpyDefault, s));
+    BCU(S.get(&d_y, n));
+    BCU(S.get(&d_npos, 1));
+    BCU(cudaMemsetAsync(d_npos, 0, sizeof(int), s));
+    {
+      const int tok = prof_begin(PK_AUX, s);
+      labels_from_betas<<<(n + 255) / 256, 256, 0, s>>>(d_b, n, d_y, d_npos);
+      prof_end(tok, s);
+    }
+    BCU(cudaMemcpyAsync(&npos, d_npos, sizeof(int), cudaMemcpyDeviceToHost, s));
     BCU(cudaStreamSynchronize(s));
-    *out_count = count;
-    if (count > 0) {
-      BCU(cudaMemcpyAsync(out_feat, d_feat, sizeof(int) * count, cudaMemcpyDefault, s));
-      BCU(cudaMemcpyAsync(out_thr, d_thr, sizeof(double) * count, cudaMemcpyDefault, s));
-      BCU(cudaMemcpyAsync(out_pol, d_pol, sizeof(double) * count, cudaMemcpyDefault, s));
-      BCU(cudaMemcpyAsync(out_alpha, d_alpha, sizeof(double) * count, cudaMemcpyDefault, s));
-      BCU(cudaMemcpyAsync(out_err, d_rerr, sizeof(double) * count, cudaMemcpyDefault, s));
-      *out_intercept = 0.0;
-      count_transfer(0, (sizeof(int) + 4 * sizeof(double)) * count);
+    if (!raw && (npos == 0 || npos == n)) {
+      // one class: zero-round ensemble carrying the class sign (boosting.py:185-187)
+      *out_count = 0;
+      *out_intercept = npos == n ? 1.0 : -1.0;
+      goto done;
+    }
+    BCU(S.get(&d_xt, (size_t)n * F));
+    BCU(S.get(&d_xsorted, (size_t)n * F));
+    BCU(S.get(&d_iota, n));
+    BCU(S.get(&d_order, (size_t)n * F));
+    {
+      const int tok = prof_begin(PK_AUX, s);
+      transpose_cols<<<(unsigned)(((int64_t)n * F + 255) / 256), 256, 0, s>>>(d_xs, n, F, d_xt, d_iota);
+      prof_end(tok, s);
+    }
+    // stable LSD radix sort of each column: ties keep index order, as np.argsort(kind="stable")
+    BCU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_xt, d_xsorted, d_iota, d_order, n, 0, 64, s));
+    BCU(S.get(reinterpret_cast<char **>(&d_tmp), tmp_bytes));
+    for (int f = 0; f < F; ++f)
+      BCU(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_xt + (size_t)f * n, d_xsorted + (size_t)f * n, d_iota,
+                                          d_order + (size_t)f * n, n, 0, 64, s));
+    BCU(S.get(&d_pid, (size_t)n * F));
+    BCU(S.get(&d_nid, (size_t)n * F));
+    BCU(S.get(&d_cnt, (size_t)n * F));
+    {
+      const int tok = prof_begin(PK_AUX, s);
+      split_classes<<<F, 256, 0, s>>>(d_order, d_y, n, d_pid, d_nid, d_cnt);
+      prof_end(tok, s);
+    }
+    BCU(S.get(&d_w, n));
+    if (weights) {
+      BCU(cudaMemcpyAsync(d_w, weights, sizeof(double) * n, cudaMemcpyDefault, s));
     } else {
-      // no stump beat random guessing: majority sign (boosting.py:202-205)
-      *out_intercept = 2 * npos >= n ? 1.0 : -1.0;
+      const int tok = prof_begin(PK_AUX, s);
+      fill_value<<<(n + 255) / 256, 256, 0, s>>>(d_w, n, 1.0 / n);
+      prof_end(tok, s);
+    }
+    BCU(S.get(&d_wn, (size_t)n * F));
+    BCU(S.get(&d_pc, (size_t)n * F));
+    BCU(S.get(&d_nc, (size_t)n * F));
+    BCU(S.get(&d_err, F));
+    BCU(S.get(&d_pos, F));
+    BCU(S.get(&d_wsub, (size_t)n * F));
+    BCU(S.get(&d_feat, rounds));
+    BCU(S.get(&d_thr, rounds));
+    BCU(S.get(&d_pol, rounds));
+    BCU(S.get(&d_alpha, rounds));
+    BCU(S.get(&d_rerr, rounds));
+    BCU(S.get(&d_count, 1));
+    root = pw_tree(n, tree);
+    BCU(S.get(&d_leaves, tree.leaves.size()));
+    BCU(cudaMemcpyAsync(d_leaves, tree.leaves.data(), sizeof(int2) * tree.leaves.size(), cudaMemcpyHostToDevice, s));
+    BCU(S.get(&d_children, tree.children.size()));
+    if (!tree.children.empty())
+      BCU(cudaMemcpyAsync(d_children, tree.children.data(), sizeof(int2) * tree.children.size(),
+                          cudaMemcpyHostToDevice, s));
+    BCU(S.get(&d_lvl, tree.level_end.size()));
+    if (!tree.level_end.empty())
+      BCU(cudaMemcpyAsync(d_lvl, tree.level_end.data(), sizeof(int) * tree.level_end.size(), cudaMemcpyHostToDevice,
+                          s));
+    {
+      BoostParams P{};
+      P.n = n;
+      P.F = F;
+      P.rounds = rounds;
+      P.raw = raw ? 1 : 0;
+      P.n_pos = npos;
+      P.xs = d_xs;
+      P.xsorted = d_xsorted;
+      P.y = d_y;
+      P.w = d_w;
+      P.wn = d_wn;
+      P.pos_idx = d_pid;
+      P.neg_idx = d_nid;
+      P.cntpos = d_cnt;
+      P.pcum = d_pc;
+      P.ncum = d_nc;
+      P.leaves = d_leaves;
+      P.n_leaves = (int)tree.leaves.size();
+      P.children = d_children;
+      P.level_end = d_lvl;
+      P.n_levels = (int)tree.level_end.size();
+      P.root = root;
+      P.feat_err = d_err;
+      P.feat_pos = d_pos;
+      P.wsub = d_wsub;
+      P.out_feat = d_feat;
+      P.out_thr = d_thr;
+      P.out_pol = d_pol;
+      P.out_alpha = d_alpha;
+      P.out_err = d_rerr;
+      P.out_count = d_count;
+      const size_t smem = sizeof(double) * (2 * tree.leaves.size() + 4 * kTile);
+      BCU(cudaFuncSetAttribute(boost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      void *args[] = {&P};
+      const int tok = prof_begin(PK_BOOST, s);
+      BCU(cudaLaunchCooperativeKernel((void *)boost_kernel, dim3(F), dim3(kBoostThreads), args, smem, s));
+      prof_end(tok, s);
+    }
+    BCU(cudaGetLastError());
+    {
+      int count = 0;
+      BCU(cudaMemcpyAsync(&count, d_count, sizeof(int), cudaMemcpyDeviceToHost, s));
+      BCU(cudaStreamSynchronize(s));
+      *out_count = count;
+      if (count > 0) {
+        BCU(cudaMemcpyAsync(out_feat, d_feat, sizeof(int) * count, cudaMemcpyDefault, s));
+        BCU(cudaMemcpyAsync(out_thr, d_thr, sizeof(double) * count, cudaMemcpyDefault, s));
+        BCU(cudaMemcpyAsync(out_pol, d_pol, sizeof(double) * count, cudaMemcpyDefault, s));
+        BCU(cudaMemcpyAsync(out_alpha, d_alpha, sizeof(double) * count, cudaMemcpyDefault, s));
+        BCU(cudaMemcpyAsync(out_err, d_rerr, sizeof(double) * count, cudaMemcpyDefault, s));
+        *out_intercept = 0.0;
+        count_transfer(0, (sizeof(int) + 4 * sizeof(double)) * count);
+      } else {
+        // no stump beat random guessing: majority sign (boosting.py:202-205)
+        *out_intercept = 2 * npos >= n ? 1.0 : -1.0;
+      }
     }
   }
 done:
-  for (void *p : {(void *)d_xs, (void *)d_b, (void *)d_xt, (void *)d_xsorted, (void *)d_y, (void *)d_w, (void *)d_pc,
-                  (void *)d_nc, (void *)d_err, (void *)d_wsub, (void *)d_thr, (void *)d_pol, (void *)d_alpha,
-                  (void *)d_rerr, (void *)d_iota, (void *)d_order, (void *)d_pos, (void *)d_npos, (void *)d_feat,
-                  (void *)d_count, (void *)d_leaves, d_tmp})
-    if (p) cudaFreeAsync(p, s);
   cudaStreamSynchronize(s);
   if (prev >= 0) cudaSetDevice(prev);
   return rc;

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -412,6 +413,42 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
   std::vector<double> ap(ns);
   for (int t = 0; t < ns; ++t) ap[t] = alpha[t] * pol[t];  // the product the reference forms per vote
   h.o_ap = put(ap, 1);
+  // per (date, feature) step tables of the stump score (see cmc_stop in brm_model.cuh)
+  const int nfeat = d > 1 ? d + 1 : 1;
+  h.nfeat = nfeat;
+  std::vector<double> tt, tv, bound(nd + 1, 0.0);
+  std::vector<int32_t> toff((size_t)(nd + 1) * nfeat, 0), tcnt((size_t)(nd + 1) * nfeat, 0),
+      voff((size_t)(nd + 1) * nfeat, 0);
+  for (int m = 0; m <= nd; ++m) {
+    const int t0 = rl->kind == BRM_RULE_CMC ? starts[m] : 0, cnt = rl->kind == BRM_RULE_CMC ? counts[m] : 0;
+    double absum = rl->kind == BRM_RULE_CMC ? std::fabs(icept[m]) : 0.0;
+    for (int f = 0; f < nfeat; ++f) {
+      std::vector<double> u;
+      for (int t = t0; t < t0 + cnt; ++t)
+        if (feat[t] == f) u.push_back(thr[t]);
+      std::sort(u.begin(), u.end());
+      u.erase(std::unique(u.begin(), u.end()), u.end());
+      const size_t idx = (size_t)m * nfeat + f;
+      toff[idx] = (int32_t)tt.size();
+      tcnt[idx] = (int32_t)u.size();
+      voff[idx] = (int32_t)tv.size();
+      tt.insert(tt.end(), u.begin(), u.end());
+      for (size_t c = 0; c <= u.size(); ++c) {
+        long double acc = 0.0L;  // votes when exactly c thresholds of f lie below x
+        for (int t = t0; t < t0 + cnt; ++t) {
+          if (feat[t] != f) continue;
+          const size_t rank = std::lower_bound(u.begin(), u.end(), thr[t]) - u.begin();
+          acc += rank < c ? (long double)ap[t] : -(long double)ap[t];
+        }
+        tv.push_back((double)acc);
+      }
+    }
+    for (int t = t0; t < t0 + cnt; ++t) absum += std::fabs(ap[t]);
+    bound[m] = 4.0 * (double)(cnt + nfeat + 4) * std::ldexp(absum, -53) + 1e-300;
+  }
+  h.o_tt = put(tt, 1);
+  h.o_tv = put(tv, 1);
+  h.o_bound = put(bound, nd + 1);
   h.n_dbl = (int)dbl.size();
   std::vector<int32_t> ints;
   auto puti = [&](const std::vector<int32_t> &v, size_t min_len) {
@@ -423,6 +460,9 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
   h.o_starts = puti(starts, nd + 1);
   h.o_counts = puti(counts, nd + 1);
   h.o_feat = puti(feat, 1);
+  h.o_toff = puti(toff, 1);
+  h.o_tcnt = puti(tcnt, 1);
+  h.o_voff = puti(voff, 1);
   h.n_int = (int)ints.size();
 
   brm_ctx *c = new brm_ctx();

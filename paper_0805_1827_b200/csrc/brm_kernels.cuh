@@ -24,6 +24,10 @@ namespace brm {
 // ---------------------------------------------------------------- walk ----
 template <int D, bool FAST>
 __global__ void __launch_bounds__(kWalkThreads) walk_units(WalkParams P) {
+  constexpr int TG = FAST ? 1 : TailGroup<D>::G;
+  __shared__ double s_tq_buf[(kWalkThreads / 32) * 32 * TG];
+  __shared__ unsigned short s_tq_idx[(kWalkThreads / 32) * 32 * TG];
+  const TailQueue tq{s_tq_buf + (threadIdx.x >> 5) * 32 * TG, s_tq_idx + (threadIdx.x >> 5) * 32 * TG};
   using R = RealT<FAST>;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double s_red[2 * (kWalkThreads / 32)];
@@ -58,7 +62,7 @@ __global__ void __launch_bounds__(kWalkThreads) walk_units(WalkParams P) {
       double *pout = P.path_out ? P.path_out + (size_t)u * P.per_unit : nullptr;
       int32_t *sout = P.stop_out ? P.stop_out + (size_t)u * P.per_unit : nullptr;
       walk_paths<D, FAST>(M, s_start, P.m_start, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, pout,
-                          sout, P.steps);
+                          sout, P.steps, tq);
     }
     __syncthreads();
     double s = 0.0, q = 0.0;
@@ -100,6 +104,10 @@ __device__ inline double probe_state(const ModelHdr &h, const double *seed, int 
 
 template <int D, bool FAST>
 __global__ void __launch_bounds__(kWalkThreads) iz_probes(IzParams P) {
+  constexpr int TG = FAST ? 1 : TailGroup<D>::G;
+  __shared__ double s_tq_buf[(kWalkThreads / 32) * 32 * TG];
+  __shared__ unsigned short s_tq_idx[(kWalkThreads / 32) * 32 * TG];
+  const TailQueue tq{s_tq_buf + (threadIdx.x >> 5) * 32 * TG, s_tq_idx + (threadIdx.x >> 5) * 32 * TG};
   using R = RealT<FAST>;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -164,7 +172,7 @@ __global__ void __launch_bounds__(kWalkThreads) iz_probes(IzParams P) {
     const uint64_t base0 = unit_base<FAST>(draw_base, P.normals != nullptr);
     if (p0 < p1)
       walk_paths<D, FAST>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, nullptr,
-                          nullptr, P.steps);
+                          nullptr, P.steps, tq);
     __syncthreads();
     double s = 0.0, q = 0.0;
     fold_values(vals, p1 > p0 ? p1 - p0 : 0, s_red, s, q);
