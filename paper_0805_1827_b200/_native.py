@@ -129,10 +129,16 @@ def f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: torch's default stream has handle 0
+
+
 def stream_handle(stream) -> C.c_void_p | None:
-    """cudaStream_t of a torch.cuda.Stream / raw int / None (legacy default stream)."""
+    """cudaStream_t of a torch.cuda.Stream / raw handle.  None -> library default;
+    a stream whose handle is 0 (torch's default stream) -> cudaStreamLegacy."""
+    if stream is None:
+        return None
     raw = getattr(stream, "cuda_stream", stream)
-    return C.c_void_p(raw) if raw else None
+    return C.c_void_p(raw if raw else CUDA_STREAM_LEGACY)
 
 
 def device_count() -> int:

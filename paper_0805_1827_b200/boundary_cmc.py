@@ -165,6 +165,15 @@ def label_points(params, spec, points, m: int, n_label: int, later: CmcRule, see
                                 db, mode=mode)
 
 
+def _torch_cuda():
+    """torch when a CUDA device is visible (device-resident buffers), else None."""
+    try:
+        import torch
+        return torch if torch.cuda.is_available() else None
+    except ImportError:
+        return None
+
+
 def build_cmc_rule(params, spec, cfg: CmcBuildConfig, seed: int = 0, engine=None, backend=None, *,
                    sampler: str = "bridge", mode=None) -> tuple[CmcRule, CmcBuildReport]:
     """Fit the per-date classifiers by backward induction (boundary_cmc.py:230-281)."""
@@ -178,28 +187,28 @@ def build_cmc_rule(params, spec, cfg: CmcBuildConfig, seed: int = 0, engine=None
     call_like = is_call_like(spec.payoff_kind)
     rule = CmcRule.empty(d, spec.n_dates, call_like)
     report = CmcBuildReport()
-    torch = None
-    if shard.distributed:
-        import torch
+    torch = _torch_cuda()
+    stream = torch.cuda.current_stream() if torch is not None else None
     for m in range(spec.n_dates - 1, 0, -1):
         later = rule.pack()
         bridge = bridge_scalars(params, spec, m)
         t0 = time.perf_counter()
-        if shard.distributed:
-            lo, hi = shard.range(cfg.n_train)
+        lo, hi = shard.range(cfg.n_train)
+        if torch is not None:
+            # device-resident date step: features and labels stay in HBM, every
+            # launch (sampler, walker, AdaBoost) is ordered on torch's stream
+            get_context(mp, later, mode=mode).set_stream(stream)
             feats = torch.empty((hi - lo, F), dtype=torch.float64, device="cuda")
             betas = torch.empty((hi - lo,), dtype=torch.float64, device="cuda")
-            get_context(mp, later, mode=mode).set_stream(torch.cuda.current_stream())
             if hi > lo:
                 _be.cmc_calc(mp, later, m, seed, lo, hi - lo, cfg.n_label, bridge, sampler, feats, betas, mode=mode)
             feats = shard.all_gather_rows(feats, cfg.n_train)
             betas = shard.all_gather_rows(betas, cfg.n_train)
-            torch.cuda.current_stream().synchronize()
         else:
             feats, betas = _be.cmc_calc(mp, later, m, seed, 0, cfg.n_train, cfg.n_label, bridge, sampler, mode=mode)
         calc_s = time.perf_counter() - t0
         t0 = time.perf_counter()
-        f, t, p, a, _, icept = _be.fit_ensemble_arrays(feats, betas, cfg.boost_rounds, mode=mode)
+        f, t, p, a, _, icept = _be.fit_ensemble_arrays(feats, betas, cfg.boost_rounds, mode=mode, stream=stream)
         ens = ensemble_from_arrays(F, f, t, p, a, icept)
         class_s = time.perf_counter() - t0
         pos = float((betas > 0).double().mean().item()) if torch is not None else float(np.mean(betas > 0.0))

@@ -90,8 +90,7 @@ class Context:
 
     def set_stream(self, stream) -> None:
         """Launch on a caller stream (a torch.cuda.Stream, raw handle, or None)."""
-        raw = getattr(stream, "cuda_stream", stream)
-        N.check(N.lib.brm_ctx_set_stream(self.handle, C.c_void_p(raw) if raw else None))
+        N.check(N.lib.brm_ctx_set_stream(self.handle, N.stream_handle(stream)))
 
     def supply_normals(self, normals, base: int = 0) -> None:
         """Fixed-input mode: draw i of every stream reads normals[i - base]."""

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -173,6 +174,19 @@ int fetch(const T *src, size_t count, std::vector<T> &dst, const char *name) {
 
 int quad_basis_size(int k) { return 1 + k + k * (k + 1) / 2; }
 
+// Library stream of a device (created once, non-blocking, never destroyed).
+cudaStream_t device_stream(int dev) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    streams[dev] = nullptr;
+  }
+  return streams[dev];
+}
+
 }  // namespace
 
 struct brm_ctx {
@@ -187,6 +201,7 @@ struct brm_ctx {
   DevInfo info;
   KernelTriple kern{};
   double *normals = nullptr;  // supplied-normals copy (device)
+  cudaEvent_t ready = nullptr;  // image upload complete (waited on by every launch stream)
   uint64_t nrm_base = 0, nrm_count = 0;
   cudaStream_t stream() const { return has_user_stream ? user_stream : own_stream; }
   bool fast() const { return mode == BRM_MODE_FAST; }
@@ -473,11 +488,18 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
   c->kern = kernels_for(d, mode == BRM_MODE_FAST);
   c->blob_bytes = 8 * dbl.size() + 4 * ints.size();
   count_transfer(c->blob_bytes, 0);
-  cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMalloc(&c->blob, c->blob_bytes);
-  if (e == cudaSuccess) e = cudaMemcpy(c->blob, dbl.data(), 8 * dbl.size(), cudaMemcpyHostToDevice);
+  // one non-blocking stream per device shared by its contexts; the image is a
+  // stream-ordered allocation, so creating and dropping contexts never syncs the device
+  c->own_stream = device_stream(device);
+  cudaError_t e = c->own_stream ? cudaSuccess : cudaErrorUnknown;
+  if (e == cudaSuccess) e = cudaMallocAsync(&c->blob, c->blob_bytes, c->own_stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c->blob, dbl.data(), 8 * dbl.size(), cudaMemcpyHostToDevice, c->own_stream);
   if (e == cudaSuccess && !ints.empty())
-    e = cudaMemcpy(c->blob + 8 * dbl.size(), ints.data(), 4 * ints.size(), cudaMemcpyHostToDevice);
+    e = cudaMemcpyAsync(c->blob + 8 * dbl.size(), ints.data(), 4 * ints.size(), cudaMemcpyHostToDevice,
+                        c->own_stream);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(c->ready, c->own_stream);
   if (e != cudaSuccess) {
     brm_ctx_destroy(c);
     return fail(e == cudaErrorMemoryAllocation ? BRM_ENOMEM : BRM_ECUDA, "context upload: %s", cudaGetErrorString(e));
@@ -493,11 +515,12 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
 int brm_ctx_destroy(brm_ctx *c) {
   if (!c) return BRM_OK;
   DeviceScope scope(c->device);
-  if (c->own_stream) cudaStreamSynchronize(c->own_stream);
-  if (c->has_user_stream) cudaStreamSynchronize(c->user_stream);
-  if (c->blob) cudaFree(c->blob);
-  if (c->normals) cudaFree(c->normals);
-  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  // freed in stream order after every launch that used the image
+  const cudaStream_t s = c->stream();
+  if (c->blob) cudaFreeAsync(c->blob, s);
+  if (c->normals) cudaFreeAsync(c->normals, s);
+  if (c->ready) cudaEventDestroy(c->ready);
+  cudaGetLastError();
   delete c;
   return BRM_OK;
 }
@@ -512,13 +535,13 @@ int brm_ctx_set_stream(brm_ctx *c, void *s) {
 int brm_ctx_supply_normals(brm_ctx *c, const double *normals, uint64_t base, uint64_t count) {
   if (!c) return fail(BRM_EINVAL, "NULL context");
   DeviceScope scope(c->device);
-  BRM_CUDA(cudaStreamSynchronize(c->stream()));
-  if (c->normals) cudaFree(c->normals);
+  if (c->normals) cudaFreeAsync(c->normals, c->stream());
   c->normals = nullptr;
   c->nrm_base = c->nrm_count = 0;
   if (!normals || count == 0) return BRM_OK;
-  BRM_CUDA(cudaMalloc(&c->normals, count * sizeof(double)));
-  BRM_CUDA(cudaMemcpy(c->normals, normals, count * sizeof(double), cudaMemcpyDefault));
+  BRM_CUDA(cudaMallocAsync(&c->normals, count * sizeof(double), c->stream()));
+  BRM_CUDA(cudaMemcpyAsync(c->normals, normals, count * sizeof(double), cudaMemcpyDefault, c->stream()));
+  BRM_CUDA(cudaStreamSynchronize(c->stream()));
   c->nrm_base = base;
   c->nrm_count = count;
   return BRM_OK;
@@ -576,6 +599,7 @@ int brm_stopped_sums(brm_ctx *c, const double *start, int32_t m_start, int64_t n
   if (n_paths < 0 || n_paths > (int64_t)1 << 30) return fail(BRM_EINVAL, "n_paths %lld out of range", (long long)n_paths);
   DeviceScope scope(c->device);
   Call call(c->stream());
+  BRM_CUDA(cudaStreamWaitEvent(call.stream, c->ready, 0));
   const double *st;
   BRM_TRY(call.in(start, c->hdr.d, &st));
   if (!st) return fail(BRM_EINVAL, "start_values is NULL");
@@ -619,6 +643,7 @@ int brm_path_values(brm_ctx *c, const double *start, int32_t m_start, int64_t n_
   if (n_paths == 0) return BRM_OK;
   DeviceScope scope(c->device);
   Call call(c->stream());
+  BRM_CUDA(cudaStreamWaitEvent(call.stream, c->ready, 0));
   const double *st;
   BRM_TRY(call.in(start, c->hdr.d, &st));
   if (!st) return fail(BRM_EINVAL, "start_values is NULL");
@@ -649,6 +674,7 @@ int brm_decisions(brm_ctx *c, const double *states, int64_t n, int32_t m, int32_
   if (n <= 0) return BRM_OK;
   DeviceScope scope(c->device);
   Call call(c->stream());
+  BRM_CUDA(cudaStreamWaitEvent(call.stream, c->ready, 0));
   DecisionParams P{};
   P.hdr = c->hdr;
   P.blob = c->blob;
@@ -680,6 +706,7 @@ int brm_price_blocks(brm_ctx *c, int64_t n_paths, uint64_t seed, int64_t block_l
   if (block_hi == block_lo) return BRM_OK;
   DeviceScope scope(c->device);
   Call call(c->stream());
+  BRM_CUDA(cudaStreamWaitEvent(call.stream, c->ready, 0));
   double *o;
   BRM_TRY(call.out(out_stats, 3 * (size_t)(block_hi - block_lo), &o));
   WalkJob j;
@@ -709,6 +736,7 @@ int brm_cmc_labels(brm_ctx *c, const double *points, int64_t n, int32_t m, int32
   if (n == 0) return BRM_OK;
   DeviceScope scope(c->device);
   Call call(c->stream());
+  BRM_CUDA(cudaStreamWaitEvent(call.stream, c->ready, 0));
   WalkJob j;
   BRM_TRY(call.in(points, (size_t)n * c->hdr.d, &j.starts));
   if (!j.starts) return fail(BRM_EINVAL, "points is NULL");
@@ -745,6 +773,7 @@ int brm_sample_points(brm_ctx *c, int32_t mode, int32_t m, uint64_t seed, int64_
   if (n <= 0) return BRM_OK;
   DeviceScope scope(c->device);
   Call call(c->stream());
+  BRM_CUDA(cudaStreamWaitEvent(call.stream, c->ready, 0));
   SampleParams P{};
   P.mode = mode;
   P.m = m;
@@ -784,6 +813,7 @@ int brm_cmc_calc(brm_ctx *c, int32_t sampler, int32_t m, uint64_t seed, int64_t 
   if (n == 0) return BRM_OK;
   DeviceScope scope(c->device);
   Call call(c->stream());
+  BRM_CUDA(cudaStreamWaitEvent(call.stream, c->ready, 0));
   const int d = c->hdr.d, F = d > 1 ? d + 1 : 1;
   SampleParams S{};
   S.mode = sampler;
@@ -849,6 +879,7 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   if (n > (1 << 20)) return fail(BRM_EINVAL, "too many probes");
   DeviceScope scope(c->device);
   Call call(c->stream());
+  BRM_CUDA(cudaStreamWaitEvent(call.stream, c->ready, 0));
   IzParams P{};
   P.hdr = c->hdr;
   P.blob = c->blob;
