@@ -64,9 +64,9 @@ class Shard:
         shape = (width,) + tuple(local.shape[1:])
         pad = torch.zeros(shape, dtype=local.dtype, device=local.device)
         pad[:local.shape[0]] = local
-        out = torch.empty((self.world,) + shape, dtype=local.dtype, device=local.device)
-        dist.all_gather_into_tensor(out, pad, group=self.group)
-        return torch.cat([out[r, :hi - lo] for r, (lo, hi) in enumerate(ranges)], dim=0)
+        parts = [torch.empty(shape, dtype=local.dtype, device=local.device) for _ in range(self.world)]
+        dist.all_gather(parts, pad, group=self.group)
+        return torch.cat([parts[r][:hi - lo] for r, (lo, hi) in enumerate(ranges)], dim=0)
 
     def all_reduce_sum(self, t):
         if self.distributed:
