@@ -118,6 +118,10 @@ int brm_raw_uint64(int32_t device, uint64_t key64, uint64_t stream64, uint64_t s
 int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t start, int64_t count,
                 double *out);
 
+/* Self-test of the walker's branch-free fp64 exp / divide against CUDA's
+ * exp / __ddiv_rn (kind 0 exp_nb(a), 1 exp(a), 2 div_nb(a, b), 3 a / b). */
+int brm_selftest_math(int32_t device, int32_t kind, const double *a, const double *b, int64_t n, double *out);
+
 /* ---- Path walker ------------------------------------------------------- */
 /* stopped_sums (core_backend.py:36-41, _core.pyx:402-430). */
 int brm_stopped_sums(brm_ctx *ctx, const double *start_values, int32_t m_start, int64_t n_paths,

@@ -54,6 +54,7 @@ _SIGNATURES = {
     "brm_derive_words": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, _up, _up]),
     "brm_raw_uint64": (C.c_int, [C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_void_p]),
     "brm_normals": (C.c_int, [C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_void_p]),
+    "brm_selftest_math": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "brm_stopped_sums": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_uint64,
                                    C.c_uint64, C.c_void_p, C.c_void_p]),
     "brm_path_values": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_uint64,

@@ -22,6 +22,9 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
 #include <cmath>
 #include <string>
@@ -29,13 +32,14 @@
 
 #include "../../include/bermuda_b200.h"
 #include "brm_internal.h"
+#include "brm_rng.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace brm {
 
 constexpr int kBoostThreads = 256;
-constexpr int kTile = 2048;
+constexpr int kTile = 4096;
 constexpr int kPwBlock = 128;  // numpy PW_BLOCKSIZE
 
 // numpy pairwise_sum leaf (n <= 128): 8 strided accumulators, fixed combine,
@@ -152,6 +156,7 @@ struct BoostParams {
   const int *pos_idx;      // [F][n] sample ids of the positives in sorted order (first n_pos[f])
   const int *neg_idx;      // [F][n] sample ids of the negatives in sorted order
   const int *cntpos;       // [F][n] positives among sorted positions 0..i
+  const int2 *brk;         // [F][n] chain indices at split i (INT_MIN: no break after i)
   double *pcum, *ncum;     // [F][n] prefix sums of the positive / negative chains
   const int2 *leaves;
   int n_leaves;
@@ -166,13 +171,34 @@ struct BoostParams {
   int *out_count;
   int n_pos;
   int raw;  // 1: one fit_stump search with the given weights, no boosting rules
+  long long *timing;  // optional per-phase clock64 totals of CTA 0 (diagnostics)
 };
 
 // CTA-wide numpy-order sum of a[0..n) (a divided by `div` on the fly when
 // div != 1); every thread gets the result.  s_node holds L + I doubles.
 __device__ double cta_pairwise(const BoostParams &P, const double *a, double *s_node) {
   const int L = P.n_leaves;
-  for (int l = threadIdx.x; l < L; l += blockDim.x) s_node[l] = pw_leaf(a + P.leaves[l].x, P.leaves[l].y);
+  // leaves: 8 lanes per leaf, lane j owns numpy's accumulator r[j] (elements
+  // j, j+8, ...); pair sums by shuffles are exact (IEEE addition commutes), the
+  // tail of len % 8 elements is added in order by the group's first lane
+  const int lane = threadIdx.x & 31, grp = lane >> 3, j = lane & 7;
+  const int groups = (blockDim.x >> 5) * 4;
+  for (int l0 = (threadIdx.x >> 5) * 4; l0 < L; l0 += groups) {
+    const int l = l0 + grp;
+    const bool ok = l < L;
+    const int off = ok ? P.leaves[l].x : 0, len = ok ? P.leaves[l].y : 0;
+    const int main = len >= 8 ? len - (len % 8) : 0;
+    double r = main ? a[off + j] : 0.0;
+    for (int i = 8; i < main; i += 8) r = __dadd_rn(r, a[off + i + j]);
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (ok && j == 0) {
+      double res = main ? r : 0.0;
+      for (int i = main; i < len; ++i) res = __dadd_rn(res, a[off + i]);
+      s_node[l] = res;
+    }
+  }
   __syncthreads();
   int lo = 0;
   for (int h = 0; h < P.n_levels; ++h) {
@@ -232,10 +258,10 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *s_node = reinterpret_cast<double *>(smem_raw);               // [L + I]
-  double *s_in_p = s_node + 2 * P.n_leaves;                            // [kTile]
-  double *s_in_n = s_in_p + kTile;                                     // [kTile]
-  double *s_out_p = s_in_n + kTile;                                    // [kTile]
-  double *s_out_n = s_out_p + kTile;                                   // [kTile]
+  double *s_in_p = s_node + 2 * P.n_leaves;
+  double *s_in_n = s_in_p + kTile;
+  double *s_out_p = s_in_n + kTile;
+  double *s_out_n = s_out_p + kTile;
   __shared__ Cand s_cand[kBoostThreads / 32];
   __shared__ int s_stop;
   __shared__ double s_alpha, s_thr, s_pol, s_err;
@@ -247,13 +273,16 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
   const int w_lo = blockIdx.x * slice, w_hi = min(w_lo + slice, n);
   double *wn = P.wn + (size_t)f * n;
   int count = 0;
+  long long t_mark = 0;
 
   for (int round = 0; round < P.rounds; ++round) {
+    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) t_mark = clock64();
     // ---- w / w.sum() (numpy pairwise order), CTA-private copy ------------
     const double s = round == 0 ? 1.0 : cta_pairwise(P, P.w, s_node);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) wn[i] = round == 0 ? P.w[i] : __ddiv_rn(P.w[i], s);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) wn[i] = round == 0 ? P.w[i] : div_nb(P.w[i], s);
     __syncthreads();
     const double total = cta_pairwise(P, wn, s_node);
+    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[1] += now - t_mark; t_mark = now; }
     // ---- split search on feature f -------------------------------------
     if (f < F) {
       const int *pid = P.pos_idx + (size_t)f * n;
@@ -262,32 +291,50 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
       double *nc = P.ncum + (size_t)f * n;
       const int n_pos = P.n_pos, n_neg = n - P.n_pos;
       double pacc = 0.0, nacc = 0.0;  // np.cumsum(where(y>0, w, 0)): zeros never change a partial sum
+      // tiles: all threads gather, the two highest warps run the two sequential
+      // chains (the issue arbiter favours high warp ids), all threads write back
+      const int chain_p = blockDim.x - 64, chain_n = blockDim.x - 32;
       for (int t0 = 0; t0 < max(n_pos, n_neg); t0 += kTile) {
         const int tp = max(0, min(kTile, n_pos - t0)), tn = max(0, min(kTile, n_neg - t0));
         for (int j = threadIdx.x; j < tp; j += blockDim.x) s_in_p[j] = wn[pid[t0 + j]];
         for (int j = threadIdx.x; j < tn; j += blockDim.x) s_in_n[j] = wn[nid[t0 + j]];
         __syncthreads();
-        if (threadIdx.x == 0) serial_chain(s_in_p, s_out_p, tp, pacc);
-        else if (threadIdx.x == 32) serial_chain(s_in_n, s_out_n, tn, nacc);
+        if (threadIdx.x == chain_p) serial_chain(s_in_p, s_out_p, tp, pacc);
+        else if (threadIdx.x == chain_n) serial_chain(s_in_n, s_out_n, tn, nacc);
         __syncthreads();
         for (int j = threadIdx.x; j < tp; j += blockDim.x) pc[t0 + j] = s_out_p[j];
         for (int j = threadIdx.x; j < tn; j += blockDim.x) nc[t0 + j] = s_out_n[j];
       }
       __syncthreads();
-      const double *xf = P.xsorted + (size_t)f * n;
-      const int *cp = P.cntpos + (size_t)f * n;
+    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[2] += now - t_mark; t_mark = now; }
+      // split points: brk[i] = (positives up to i) - 1, (negatives up to i) - 1,
+      // precomputed once per fit; x == INT_MIN marks "no distinct-value break"
+      const int2 *brk = P.brk + (size_t)f * n;
       const double tot_neg = n_neg > 0 ? nc[n_neg - 1] : 0.0;
       Cand best{__longlong_as_double(0x7ff0000000000000LL), 0x7fffffff};
-      for (int i = threadIdx.x; i < n - 1; i += blockDim.x) {
-        if (!(__dsub_rn(xf[i + 1], xf[i]) > 0.0)) continue;
-        const int np_ = cp[i], nn_ = i + 1 - np_;
-        const double pcs = np_ > 0 ? pc[np_ - 1] : 0.0;
-        const double ncs = nn_ > 0 ? nc[nn_ - 1] : 0.0;
-        const double ep = __dadd_rn(pcs, __dsub_rn(tot_neg, ncs));
-        const double em = __dsub_rn(total, ep);
-        const Cand ca{ep, 2 * i}, cb{em, 2 * i + 1};
-        if (cand_less(ca, best)) best = ca;
-        if (cand_less(cb, best)) best = cb;
+      for (int i0 = threadIdx.x; i0 < n - 1; i0 += 4 * blockDim.x) {
+        int2 bi[4];
+        double pcs[4], ncs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * blockDim.x;
+          bi[u] = i < n - 1 ? brk[i] : make_int2(INT_MIN, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          pcs[u] = bi[u].x >= 0 ? pc[bi[u].x] : 0.0;
+          ncs[u] = bi[u].y >= 0 ? nc[bi[u].y] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (bi[u].x == INT_MIN) continue;
+          const int i = i0 + u * blockDim.x;
+          const double ep = __dadd_rn(pcs[u], __dsub_rn(tot_neg, ncs[u]));
+          const double em = __dsub_rn(total, ep);
+          const Cand ca{ep, 2 * i}, cb{em, 2 * i + 1};
+          if (cand_less(ca, best)) best = ca;
+          if (cand_less(cb, best)) best = cb;
+        }
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
@@ -305,7 +352,9 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
         P.feat_pos[f] = best.key;
       }
     }
+    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[3] += now - t_mark; t_mark = now; }
     grid.sync();
+    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[4] += now - t_mark; t_mark = now; }
     // ---- pick the winner (every CTA, same answer) ------------------------
     if (threadIdx.x == 0) {
       double be = __longlong_as_double(0x7ff0000000000000LL);
@@ -380,6 +429,7 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
     if (s_stop == 1) break;
     ++count;
     if (s_stop == 3 || round + 1 == P.rounds) break;
+    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[5] += now - t_mark; t_mark = now; }
     // ---- reweight own slice: w = (w / sum) * exp(-alpha * y * pred) ------
     {
       const double a = s_alpha, thr = s_thr, pol = s_pol;
@@ -391,14 +441,15 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
       }
     }
     grid.sync();
+    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[6] += now - t_mark; t_mark = now; }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *P.out_count = count;
 }
 
 // Per feature: ids of positives / negatives in sorted order and the running
 // count of positives (once per fit; labels and order are fixed across rounds).
-__global__ void __launch_bounds__(256) split_classes(const int *order, const double *y, int n, int *pos_idx,
-                                                     int *neg_idx, int *cntpos) {
+__global__ void __launch_bounds__(256) split_classes(const int *order, const double *y, const double *xsorted, int n,
+                                                     int *pos_idx, int *neg_idx, int *cntpos, int2 *brk) {
   using Scan = cub::BlockScan<int, 256>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_carry;
@@ -418,6 +469,10 @@ __global__ void __launch_bounds__(256) split_classes(const int *order, const dou
       cntpos[(size_t)f * n + i] = before + pos;
       if (pos) pos_idx[(size_t)f * n + before] = id;
       else neg_idx[(size_t)f * n + (i - before)] = id;
+      const double *xf = xsorted + (size_t)f * n;
+      const bool is_break = i + 1 < n && __dsub_rn(xf[i + 1], xf[i]) > 0.0;  // boosting.py:145
+      const int np_ = before + pos, nn_ = i + 1 - np_;
+      brk[(size_t)f * n + i] = is_break ? make_int2(np_ - 1, nn_ - 1) : make_int2(INT_MIN, 0);
     }
     __syncthreads();
     if (threadIdx.x == 0) s_carry = carry + tile_total;
@@ -614,7 +669,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
     double *d_xs, *d_b, *d_xt, *d_xsorted, *d_y, *d_w, *d_wn, *d_pc, *d_nc, *d_err, *d_wsub, *d_thr, *d_pol,
         *d_alpha, *d_rerr;
     int *d_iota, *d_order, *d_pos, *d_npos, *d_feat, *d_count, *d_pid, *d_nid, *d_cnt, *d_lvl;
-    int2 *d_leaves, *d_children;
+    int2 *d_leaves, *d_children, *d_brk;
     void *d_tmp = nullptr;
     size_t tmp_bytes = 0;
     int npos = 0;
@@ -660,9 +715,10 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
     BCU(S.get(&d_pid, (size_t)n * F));
     BCU(S.get(&d_nid, (size_t)n * F));
     BCU(S.get(&d_cnt, (size_t)n * F));
+    BCU(S.get(&d_brk, (size_t)n * F));
     {
       const int tok = prof_begin(PK_AUX, s);
-      split_classes<<<F, 256, 0, s>>>(d_order, d_y, n, d_pid, d_nid, d_cnt);
+      split_classes<<<F, 256, 0, s>>>(d_order, d_y, d_xsorted, n, d_pid, d_nid, d_cnt, d_brk);
       prof_end(tok, s);
     }
     BCU(S.get(&d_w, n));
@@ -711,6 +767,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       P.pos_idx = d_pid;
       P.neg_idx = d_nid;
       P.cntpos = d_cnt;
+      P.brk = d_brk;
       P.pcum = d_pc;
       P.ncum = d_nc;
       P.leaves = d_leaves;
@@ -728,12 +785,26 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       P.out_alpha = d_alpha;
       P.out_err = d_rerr;
       P.out_count = d_count;
+      long long *d_timing = nullptr;
+      const bool timing = getenv("BRM_BOOST_TIMING") != nullptr;
+      if (timing) {
+        BCU(S.get(&d_timing, 8));
+        BCU(cudaMemsetAsync(d_timing, 0, 8 * sizeof(long long), s));
+      }
+      P.timing = d_timing;
       const size_t smem = sizeof(double) * (2 * tree.leaves.size() + 4 * kTile);
       BCU(cudaFuncSetAttribute(boost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       void *args[] = {&P};
       const int tok = prof_begin(PK_BOOST, s);
       BCU(cudaLaunchCooperativeKernel((void *)boost_kernel, dim3(F), dim3(kBoostThreads), args, smem, s));
       prof_end(tok, s);
+      if (timing) {
+        long long h[8];
+        BCU(cudaMemcpyAsync(h, d_timing, sizeof h, cudaMemcpyDeviceToHost, s));
+        BCU(cudaStreamSynchronize(s));
+        fprintf(stderr, "boost phases (kcycles, CTA 0): norm+total %.0f chains %.0f scan %.0f sync1 %.0f pick %.0f reweight+sync2 %.0f\n",
+                h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, h[6] / 1e3);
+      }
     }
     BCU(cudaGetLastError());
     {

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cmath>
+#include <limits>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -406,7 +407,11 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
   for (int i = 0; i < d; ++i)
     for (int a = i + 1; a < d; ++a)
       if (chol[i * d + a] != 0.0) lower = 0;
-  h.chol_lower = lower;
+  int diag = 1;
+  for (int i = 0; i < d; ++i)
+    for (int a = 0; a < d; ++a)
+      if (a != i && chol[i * d + a] != 0.0) diag = 0;
+  h.chol_lower = diag ? 2 : lower;
   std::vector<double> dbl;
   auto put = [&](const std::vector<double> &v, size_t min_len) {
     int off = (int)dbl.size();
@@ -444,10 +449,14 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
       std::sort(u.begin(), u.end());
       u.erase(std::unique(u.begin(), u.end()), u.end());
       const size_t idx = (size_t)m * nfeat + f;
+      // padded to P-1 entries (P = power of two > count) for a fixed-trip search
+      int P = 1;
+      while (P < (int)u.size() + 1) P <<= 1;
       toff[idx] = (int32_t)tt.size();
-      tcnt[idx] = (int32_t)u.size();
+      tcnt[idx] = (int32_t)P;
       voff[idx] = (int32_t)tv.size();
       tt.insert(tt.end(), u.begin(), u.end());
+      tt.insert(tt.end(), (size_t)(P - 1) - u.size(), std::numeric_limits<double>::infinity());
       for (size_t c = 0; c <= u.size(); ++c) {
         long double acc = 0.0L;  // votes when exactly c thresholds of f lie below x
         for (int t = t0; t < t0 + cnt; ++t) {
@@ -590,6 +599,21 @@ int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t star
   BRM_TRY(call.finish());
   BRM_CUDA(cudaStreamSynchronize(call.stream));
   return BRM_OK;
+}
+
+int brm_selftest_math(int32_t device, int32_t kind, const double *a, const double *b, int64_t n, double *out) {
+  if (n <= 0) return BRM_OK;
+  if (kind < 0 || kind > 3) return fail(BRM_EINVAL, "unknown self-test %d", kind);
+  DeviceScope scope(device);
+  Call call(nullptr);
+  const double *da, *db = nullptr;
+  double *o;
+  BRM_TRY(call.in(a, n, &da));
+  if (kind >= 2) BRM_TRY(call.in(b, n, &db));
+  BRM_TRY(call.out(out, n, &o));
+  void *args[] = {&kind, &da, &db, &n, &o};
+  BRM_CUDA(cudaLaunchKernel(math_selftest_kernel(), dim3((unsigned)((n + 255) / 256)), dim3(256), args, 0, call.stream));
+  return call.finish();
 }
 
 int brm_stopped_sums(brm_ctx *c, const double *start, int32_t m_start, int64_t n_paths, uint64_t key64,

@@ -103,5 +103,6 @@ void *finish_kernel();
 void *sample_kernel();
 void *fill_raw_kernel();
 void *fill_normals_kernel();
+void *math_selftest_kernel();
 
 }  // namespace brm

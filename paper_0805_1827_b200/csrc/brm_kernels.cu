@@ -110,6 +110,18 @@ __global__ void fill_normals(uint64_t key, uint64_t stream, uint64_t start, int6
     out[i] = normal_at(key, stream, start + (uint64_t)i);
 }
 
+// Math self-test: the branch-free exp / divide against the library functions.
+__global__ void math_selftest(int kind, const double *a, const double *b, int64_t n, double *out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  switch (kind) {
+    case 0: out[i] = exp_nb(a[i]); break;
+    case 1: out[i] = exp(a[i]); break;
+    case 2: out[i] = div_nb(a[i], b[i]); break;
+    default: out[i] = __ddiv_rn(a[i], b[i]); break;
+  }
+}
+
 // ---------------------------------------------------------- dispatch tables ----
 KernelTriple kernels_d0(bool fast);
 KernelTriple kernels_d1(bool fast);
@@ -135,5 +147,6 @@ void *finish_kernel() { return (void *)&finish_units; }
 void *sample_kernel() { return (void *)&sample_points; }
 void *fill_raw_kernel() { return (void *)&fill_raw; }
 void *fill_normals_kernel() { return (void *)&fill_normals; }
+void *math_selftest_kernel() { return (void *)&math_selftest; }
 
 }  // namespace brm

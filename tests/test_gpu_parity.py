@@ -226,3 +226,26 @@ def test_lstsq_vs_numpy(k, J):
     o = O.regress(design, levels)
     assert not deficient
     assert np.allclose(design @ g, design @ o, rtol=1e-9, atol=1e-9)
+
+
+def test_branch_free_math_is_bit_identical():
+    """exp_nb / div_nb (brm_rng.cuh) return CUDA's exp / __ddiv_rn bits on the walker's ranges."""
+    from paper_0805_1827_b200 import _native as N
+    rng = np.random.default_rng(11)
+    n = 1 << 22
+    x = np.concatenate([rng.uniform(-40, 40, n), rng.normal(scale=0.3, size=n), rng.uniform(-700, 700, 1 << 16)])
+
+    def run(kind, a, b=None):
+        out = np.empty(a.size)
+        N.check(N.lib.brm_selftest_math(0, kind, N.ptr(a), N.ptr(b), a.size, N.ptr(out)))
+        return out
+
+    assert np.array_equal(run(0, x).view(np.int64), run(1, x).view(np.int64))
+    # AS241 central quotients plus generic well-scaled operands
+    q = rng.uniform(-0.425, 0.425, n)
+    r = 0.180625 - q * q
+    num = q * (3.387 + 133.1 * r + 1971.6 * r * r)
+    den = 1.0 + 42.3 * r + 687.2 * r * r
+    a = np.concatenate([num, rng.normal(size=n) * np.exp(rng.uniform(-300, 300, n))])
+    b = np.concatenate([den, rng.normal(size=n) * np.exp(rng.uniform(-300, 300, n))])
+    assert np.array_equal(run(2, a, b).view(np.int64), run(3, a, b).view(np.int64))
