@@ -14,7 +14,7 @@ from pathlib import Path
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libbermuda_b200.so"
+_LIB_PATH = Path(os.environ.get("BRM_LIB_PATH") or Path(__file__).resolve().parent / "lib" / "libbermuda_b200.so")
 
 BRM_OK, BRM_EINVAL, BRM_ENOMEM, BRM_ECUDA, BRM_ENODEV = range(5)
 MODE_PARITY, MODE_FAST = 0, 1
