@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
@@ -480,6 +481,196 @@ __global__ void __launch_bounds__(256) split_classes(const int *order, const dou
   }
 }
 
+// ---------------------------------------------------------- fast mode ----
+// BRM_MODE_FAST AdaBoost: the same stump search and boosting rules, with the
+// weights quantised to 62-bit fixed point for the split search.  Integer
+// prefix sums are exact and associative, so every prefix is a parallel block
+// scan (no sequential fp64 chain) and the result is identical for any
+// scheduling; the fp64 weights are renormalised in a fixed tree order.
+// Statistically equivalent to the reference, not bit-identical to numpy.
+constexpr double kFix = 4611686018427387904.0;  // 2^62
+
+struct FastBoostParams {
+  int n, F, rounds, raw;
+  const double *xs, *xsorted, *y;
+  const int *order;
+  double *w;                    // [n] fp64 weights (unnormalised between rounds)
+  long long *feat_err;          // [F] best integer error of each feature
+  int *feat_pos;                // [F]
+  int *out_feat;
+  double *out_thr, *out_pol, *out_alpha, *out_err;
+  int *out_count;
+};
+
+// Fixed-order CTA sum (thread-strided runs, shuffle tree, warps in order).
+__device__ double cta_sum_fixed(const double *a, int n, double *s_red) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += a[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < (int)blockDim.x / 32; ++w) t += s_red[w];
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ long long fixw(double w, double inv_s) { return __double2ll_rn(w * inv_s * kFix); }
+
+__global__ void __launch_bounds__(kBoostThreads) boost_fast_kernel(FastBoostParams P) {
+  using Scan = cub::BlockScan<long long, kBoostThreads>;
+  using Red = cub::BlockReduce<long long, kBoostThreads>;
+  __shared__ typename Scan::TempStorage s_scan;
+  __shared__ typename Red::TempStorage s_redi;
+  __shared__ double s_red[kBoostThreads / 32];
+  __shared__ long long s_tot, s_totneg, s_carry_p, s_carry_n;
+  __shared__ struct { long long err; int key; } s_cand[kBoostThreads / 32];
+  __shared__ int s_stop, s_feat;
+  __shared__ double s_thr, s_pol, s_alpha, s_err;
+  cg::grid_group grid = cg::this_grid();
+  const int n = P.n, F = P.F, f = blockIdx.x;
+  const int slice = (n + gridDim.x - 1) / gridDim.x;
+  const int w_lo = blockIdx.x * slice, w_hi = min(w_lo + slice, n);
+  int count = 0;
+  for (int round = 0; round < P.rounds; ++round) {
+    const double ssum = cta_sum_fixed(P.w, n, s_red);
+    const double inv_s = 1.0 / ssum;
+    // totals (exact)
+    long long tp = 0, tn = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const long long W = fixw(P.w[i], inv_s);
+      if (P.y[i] > 0.0) tp += W;
+      else tn += W;
+    }
+    tp = Red(s_redi).Sum(tp);
+    __syncthreads();
+    tn = Red(s_redi).Sum(tn);
+    if (threadIdx.x == 0) {
+      s_tot = tp + tn;
+      s_totneg = tn;
+      s_carry_p = s_carry_n = 0;
+    }
+    __syncthreads();
+    const long long total = s_tot, tot_neg = s_totneg;
+    // split search: one block scan per tile of sorted positions
+    long long best_err = LLONG_MAX;
+    int best_key = INT_MAX;
+    const int *ord = P.order + (size_t)f * n;
+    const double *xf = P.xsorted + (size_t)f * n;
+    constexpr int ITEMS = 8;  // consecutive sorted positions per thread per tile
+    for (int t0 = 0; t0 < n; t0 += ITEMS * blockDim.x) {
+      const int i0 = t0 + threadIdx.x * ITEMS;
+      long long wp[ITEMS], wn_[ITEMS];
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int i = i0 + k;
+        wp[k] = wn_[k] = 0;
+        if (i < n) {
+          const int id = ord[i];
+          const long long W = fixw(P.w[id], inv_s);
+          if (P.y[id] > 0.0) wp[k] = W;
+          else wn_[k] = W;
+        }
+      }
+      long long lp = 0, ln = 0;
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) lp += wp[k], ln += wn_[k];
+      long long ep_, en_, sp, sn;
+      Scan(s_scan).ExclusiveSum(lp, ep_, sp);
+      __syncthreads();
+      Scan(s_scan).ExclusiveSum(ln, en_, sn);
+      long long cp = s_carry_p + ep_, cn = s_carry_n + en_;
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        const int i = i0 + k;
+        cp += wp[k];
+        cn += wn_[k];
+        if (i < n - 1 && __dsub_rn(xf[i + 1], xf[i]) > 0.0) {
+          const long long ep = cp + (tot_neg - cn), em = total - ep;
+          if (ep < best_err || (ep == best_err && 2 * i < best_key)) best_err = ep, best_key = 2 * i;
+          if (em < best_err || (em == best_err && 2 * i + 1 < best_key)) best_err = em, best_key = 2 * i + 1;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_carry_p += sp;
+        s_carry_n += sn;
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const long long oe = __shfl_down_sync(0xffffffffu, best_err, off);
+      const int ok = __shfl_down_sync(0xffffffffu, best_key, off);
+      if (oe < best_err || (oe == best_err && ok < best_key)) best_err = oe, best_key = ok;
+    }
+    if ((threadIdx.x & 31) == 0) s_cand[threadIdx.x >> 5] = {best_err, best_key};
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)blockDim.x / 32; ++w)
+        if (s_cand[w].err < best_err || (s_cand[w].err == best_err && s_cand[w].key < best_key))
+          best_err = s_cand[w].err, best_key = s_cand[w].key;
+      P.feat_err[f] = best_err;
+      P.feat_pos[f] = best_key;
+    }
+    grid.sync();
+    if (threadIdx.x == 0) {
+      long long be = LLONG_MAX;
+      int bf = -1, bk = 0;
+      for (int g = 0; g < F; ++g)
+        if (P.feat_pos[g] != INT_MAX && P.feat_err[g] < be) be = P.feat_err[g], bf = g, bk = P.feat_pos[g];
+      if (bf < 0) {  // every feature constant: majority constant stump
+        const double pol = 2 * tot_neg <= total ? 1.0 : -1.0;  // +1 iff sum(w y) >= 0
+        s_feat = 0;
+        s_thr = __longlong_as_double(0xfff0000000000000LL);
+        s_pol = pol;
+        s_err = (double)(pol > 0 ? tot_neg : total - tot_neg) / (double)total;
+      } else {
+        const double *xb = P.xsorted + (size_t)bf * n;
+        const int i = bk >> 1;
+        s_feat = bf;
+        s_thr = 0.5 * (xb[i] + xb[i + 1]);
+        s_pol = (bk & 1) ? -1.0 : 1.0;
+        s_err = (double)be / (double)total;
+      }
+      const double err = s_err;
+      if (P.raw) {
+        if (blockIdx.x == 0) {
+          P.out_feat[0] = s_feat, P.out_thr[0] = s_thr, P.out_pol[0] = s_pol, P.out_alpha[0] = 1.0;
+          P.out_err[0] = err;
+        }
+        s_stop = 3;
+      } else if (err >= 0.5) {
+        s_stop = 1;
+      } else {
+        const double a = 0.5 * log((1.0 - err) / (err > 1e-10 ? err : 1e-10));
+        s_alpha = a;
+        if (blockIdx.x == 0) {
+          P.out_feat[count] = s_feat, P.out_thr[count] = s_thr, P.out_pol[count] = s_pol;
+          P.out_alpha[count] = a, P.out_err[count] = err;
+        }
+        s_stop = err <= 0.0 ? 3 : 0;
+      }
+    }
+    __syncthreads();
+    if (s_stop == 1) break;
+    ++count;
+    if (s_stop == 3 || round + 1 == P.rounds) break;
+    {
+      const double a = s_alpha, thr = s_thr, pol = s_pol;
+      const int feat = s_feat;
+      const double e_agree = exp(-a), e_miss = exp(a);
+      for (int i = w_lo + threadIdx.x; i < w_hi; i += blockDim.x) {
+        const double pred = P.xs[(size_t)i * F + feat] > thr ? pol : -pol;
+        P.w[i] = P.w[i] * inv_s * ((P.y[i] * pred > 0.0) ? e_agree : e_miss);
+      }
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *P.out_count = count;
+}
+
 __global__ void transpose_cols(const double *xs, int n, int F, double *xt, int *iota) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * F) return;
@@ -650,7 +841,6 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
                                 const double *betas, const double *weights, int64_t n64, int32_t F, int32_t rounds,
                                 int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha,
                                 double *out_err, int32_t *out_count, double *out_intercept) {
-  (void)mode;  // both modes replay numpy's summation orders in this build
   const bool raw = flags & BRM_FIT_SINGLE_STUMP;
   if (!xs || !betas || !out_count || !out_intercept) return bfail(BRM_EINVAL, "NULL argument");
   if (rounds < 1) return bfail(BRM_EINVAL, "need at least one round, got " + std::to_string(rounds));
@@ -796,7 +986,32 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       BCU(cudaFuncSetAttribute(boost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       void *args[] = {&P};
       const int tok = prof_begin(PK_BOOST, s);
-      BCU(cudaLaunchCooperativeKernel((void *)boost_kernel, dim3(F), dim3(kBoostThreads), args, smem, s));
+      if (mode == BRM_MODE_FAST) {
+        FastBoostParams Q{};
+        Q.n = n;
+        Q.F = F;
+        Q.rounds = rounds;
+        Q.raw = raw ? 1 : 0;
+        Q.xs = d_xs;
+        Q.xsorted = d_xsorted;
+        Q.y = d_y;
+        Q.order = d_order;
+        Q.w = d_w;
+        long long *d_ferr = nullptr;
+        BCU(S.get(&d_ferr, F));
+        Q.feat_err = d_ferr;
+        Q.feat_pos = d_pos;
+        Q.out_feat = d_feat;
+        Q.out_thr = d_thr;
+        Q.out_pol = d_pol;
+        Q.out_alpha = d_alpha;
+        Q.out_err = d_rerr;
+        Q.out_count = d_count;
+        void *qargs[] = {&Q};
+        BCU(cudaLaunchCooperativeKernel((void *)boost_fast_kernel, dim3(F), dim3(kBoostThreads), qargs, 0, s));
+      } else {
+        BCU(cudaLaunchCooperativeKernel((void *)boost_kernel, dim3(F), dim3(kBoostThreads), args, smem, s));
+      }
       prof_end(tok, s);
       if (timing) {
         long long h[8];

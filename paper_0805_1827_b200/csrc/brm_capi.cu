@@ -422,6 +422,10 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
   h.o_mu = put(mu, d);
   h.o_vol = put(vol, d);
   h.o_chol = put(chol, (size_t)d * d);
+  std::vector<double> cholT((size_t)d * d);
+  for (int i = 0; i < d; ++i)
+    for (int a = 0; a < d; ++a) cholT[(size_t)a * d + i] = chol[(size_t)i * d + a];
+  h.o_cholT = put(cholT, (size_t)d * d);
   h.o_disc = put(disc, nd + 1);
   h.o_s0 = put(s0, d);
   h.o_izc = put(izc, 1);
@@ -457,13 +461,19 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
       voff[idx] = (int32_t)tv.size();
       tt.insert(tt.end(), u.begin(), u.end());
       tt.insert(tt.end(), (size_t)(P - 1) - u.size(), std::numeric_limits<double>::infinity());
-      for (size_t c = 0; c <= u.size(); ++c) {
-        long double acc = 0.0L;  // votes when exactly c thresholds of f lie below x
-        for (int t = t0; t < t0 + cnt; ++t) {
-          if (feat[t] != f) continue;
-          const size_t rank = std::lower_bound(u.begin(), u.end(), thr[t]) - u.begin();
-          acc += rank < c ? (long double)ap[t] : -(long double)ap[t];
-        }
+      // T[c] = votes when exactly c thresholds of f lie below x:
+      //      = -sum(ap) + 2 * sum(ap of stumps with rank < c)   (long double, O(stumps))
+      std::vector<long double> by_rank(u.size(), 0.0L);
+      long double neg = 0.0L;
+      for (int t = t0; t < t0 + cnt; ++t) {
+        if (feat[t] != f) continue;
+        by_rank[std::lower_bound(u.begin(), u.end(), thr[t]) - u.begin()] += (long double)ap[t];
+        neg -= (long double)ap[t];
+      }
+      long double acc = neg;
+      tv.push_back((double)acc);
+      for (size_t r = 0; r < u.size(); ++r) {
+        acc += 2.0L * by_rank[r];
         tv.push_back((double)acc);
       }
     }

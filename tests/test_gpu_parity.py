@@ -249,3 +249,28 @@ def test_branch_free_math_is_bit_identical():
     a = np.concatenate([num, rng.normal(size=n) * np.exp(rng.uniform(-300, 300, n))])
     b = np.concatenate([den, rng.normal(size=n) * np.exp(rng.uniform(-300, 300, n))])
     assert np.array_equal(run(2, a, b).view(np.int64), run(3, a, b).view(np.int64))
+
+
+def test_fast_mode_adaboost_deterministic_and_equivalent():
+    """Fixed-point fast fit: deterministic, same first stump as the exact fit on a clear split,
+    training error within 1% of the exact fit."""
+    rng = np.random.default_rng(5)
+    n, F = 6000, 6
+    X = 100 * np.exp(0.2 * rng.normal(size=(n, F)))
+    X[:, -1] = X.max(axis=1)
+    beta = (X[:, -1] - 118) + 3 * rng.normal(size=n)
+    a = G.fit_ensemble_arrays(X, beta, 60, mode="fast")
+    b = G.fit_ensemble_arrays(X, beta, 60, mode="fast")
+    for u, v in zip(a, b):
+        assert np.array_equal(np.asarray(u), np.asarray(v))
+    p = G.fit_ensemble_arrays(X, beta, 60, mode="parity")
+    assert (a[0][0], a[1][0], a[2][0]) == (p[0][0], p[1][0], p[2][0])
+
+    def train_err(fit):
+        f, t, pol, al, _, ic = fit
+        s = np.full(n, ic)
+        for k in range(len(f)):
+            s += al[k] * np.where(X[:, f[k]] > t[k], pol[k], -pol[k])
+        return np.mean((s > 0) != (beta > 0))
+
+    assert abs(train_err(a) - train_err(p)) < 0.01
