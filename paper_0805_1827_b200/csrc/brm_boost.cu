@@ -21,6 +21,7 @@
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
 
 #include <algorithm>
 #include <climits>
@@ -190,7 +191,13 @@ __device__ double cta_pairwise(const BoostParams &P, const double *a, double *s_
     const int off = ok ? P.leaves[l].x : 0, len = ok ? P.leaves[l].y : 0;
     const int main = len >= 8 ? len - (len % 8) : 0;
     double r = main ? a[off + j] : 0.0;
-    for (int i = 8; i < main; i += 8) r = __dadd_rn(r, a[off + i + j]);
+    // leaves hold <= 128 elements: all 15 further loads of this lane are issued up front
+    double col[kPwBlock / 8 - 1];
+#pragma unroll
+    for (int q = 0; q < kPwBlock / 8 - 1; ++q) col[q] = 8 * (q + 1) < main ? a[off + 8 * (q + 1) + j] : 0.0;
+#pragma unroll
+    for (int q = 0; q < kPwBlock / 8 - 1; ++q)
+      if (8 * (q + 1) < main) r = __dadd_rn(r, col[q]);
     r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
     r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
     r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
@@ -313,21 +320,22 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
       const int2 *brk = P.brk + (size_t)f * n;
       const double tot_neg = n_neg > 0 ? nc[n_neg - 1] : 0.0;
       Cand best{__longlong_as_double(0x7ff0000000000000LL), 0x7fffffff};
-      for (int i0 = threadIdx.x; i0 < n - 1; i0 += 4 * blockDim.x) {
-        int2 bi[4];
-        double pcs[4], ncs[4];
+      constexpr int U = 8;
+      for (int i0 = threadIdx.x; i0 < n - 1; i0 += U * blockDim.x) {
+        int2 bi[U];
+        double pcs[U], ncs[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int i = i0 + u * blockDim.x;
           bi[u] = i < n - 1 ? brk[i] : make_int2(INT_MIN, 0);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
           pcs[u] = bi[u].x >= 0 ? pc[bi[u].x] : 0.0;
           ncs[u] = bi[u].y >= 0 ? nc[bi[u].y] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
           if (bi[u].x == INT_MIN) continue;
           const int i = i0 + u * blockDim.x;
           const double ep = __dadd_rn(pcs[u], __dsub_rn(tot_neg, ncs[u]));
@@ -676,7 +684,7 @@ __global__ void transpose_cols(const double *xs, int n, int F, double *xt, int *
   if (i >= (int64_t)n * F) return;
   const int r = (int)(i / F), c = (int)(i % F);
   xt[(size_t)c * n + r] = __dadd_rn(xs[i], 0.0);  // -0.0 -> +0.0: numpy sorts them as equal
-  if (c == 0) iota[r] = r;
+  iota[(size_t)c * n + r] = r;  // per-column sample ids for the segmented sort
 }
 
 __global__ void labels_from_betas(const double *betas, int n, double *y, int *npos) {
@@ -858,7 +866,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
     Scratch S(s);
     double *d_xs, *d_b, *d_xt, *d_xsorted, *d_y, *d_w, *d_wn, *d_pc, *d_nc, *d_err, *d_wsub, *d_thr, *d_pol,
         *d_alpha, *d_rerr;
-    int *d_iota, *d_order, *d_pos, *d_npos, *d_feat, *d_count, *d_pid, *d_nid, *d_cnt, *d_lvl;
+    int *d_iota, *d_order, *d_pos, *d_npos, *d_feat, *d_count, *d_pid, *d_nid, *d_cnt, *d_lvl, *d_segoff;
     int2 *d_leaves, *d_children, *d_brk;
     void *d_tmp = nullptr;
     size_t tmp_bytes = 0;
@@ -889,7 +897,8 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
     }
     BCU(S.get(&d_xt, (size_t)n * F));
     BCU(S.get(&d_xsorted, (size_t)n * F));
-    BCU(S.get(&d_iota, n));
+    BCU(S.get(&d_iota, (size_t)n * F));
+    BCU(S.get(&d_segoff, F + 1));
     BCU(S.get(&d_order, (size_t)n * F));
     {
       const int tok = prof_begin(PK_AUX, s);
@@ -897,11 +906,17 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       prof_end(tok, s);
     }
     // stable LSD radix sort of each column: ties keep index order, as np.argsort(kind="stable")
-    BCU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_xt, d_xsorted, d_iota, d_order, n, 0, 64, s));
-    BCU(S.get(reinterpret_cast<char **>(&d_tmp), tmp_bytes));
-    for (int f = 0; f < F; ++f)
-      BCU(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_xt + (size_t)f * n, d_xsorted + (size_t)f * n, d_iota,
-                                          d_order + (size_t)f * n, n, 0, 64, s));
+    {
+      // one segmented sort for all columns (segment f = column f)
+      std::vector<int> off(F + 1);
+      for (int f = 0; f <= F; ++f) off[f] = f * n;
+      BCU(cudaMemcpyAsync(d_segoff, off.data(), sizeof(int) * (F + 1), cudaMemcpyHostToDevice, s));
+      BCU(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp_bytes, d_xt, d_xsorted, d_iota, d_order, n * F, F,
+                                                   d_segoff, d_segoff + 1, 0, 64, s));
+      BCU(S.get(reinterpret_cast<char **>(&d_tmp), tmp_bytes));
+      BCU(cub::DeviceSegmentedRadixSort::SortPairs(d_tmp, tmp_bytes, d_xt, d_xsorted, d_iota, d_order, n * F, F,
+                                                   d_segoff, d_segoff + 1, 0, 64, s));
+    }
     BCU(S.get(&d_pid, (size_t)n * F));
     BCU(S.get(&d_nid, (size_t)n * F));
     BCU(S.get(&d_cnt, (size_t)n * F));
