@@ -51,10 +51,14 @@ CONFIGS = {
                n_paths=1 << 24, sampler="bridge", mode="parity"),
 }
 
-# Modelled fp64 pipe work per executed asset-step of the parity walker
-# (DP lane-instructions: AS241 central ~33 + divide ~20 + uniform 2 + step 3
-# + exp ~17 ...); see DESIGN.md "Roofline" and profiles/.
-DP_OPS_PER_ASSET_STEP = 70.0
+# fp64-pipe lane-operations per executed asset-step of the parity walker,
+# measured by ncu on the C5 label launch (DADD+DMUL+DFMA+DSETP thread
+# instructions / executed asset-steps; profiles/r01_walk_c5_sass_mix.txt):
+# AS241 central ~33 + divide ~9 + exp ~17 + uniform/step ~6 + rule compares.
+DP_OPS_PER_ASSET_STEP = 85.4
+# DRAM bytes per walker launch from the same capture (dram__bytes_read+write,
+# profiles/r01_walk_c5_labels_pricing.txt): label launch 995.6 KB, pricing 112.9 KB
+WALK_DRAM_BYTES_PER_LAUNCH = (995.6e3 + 112.9e3) / 2
 FP64_LANES_PER_SM = 64
 N_SMS = 148
 
@@ -197,6 +201,23 @@ def run_engine(args, cfg):
             barrier()
     N.profile_enable(False)
     prof = N.profile_read()
+    alt = None
+    if cfg["method"] == "cmc" and mode == "parity" and not args.no_fast_line:
+        # the same workload in fast mode (fp32 Box-Muller stepping, fixed-point AdaBoost), for reference
+        engine_step(cfg, E, params, spec, "fast")
+        ts = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.zero_()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            est_f, _, _ = engine_step(cfg, E, params, spec, "fast")
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms_f = float(np.mean(ts))
+        alt = {"mode": "fast", "dtype": "f32-step/f64-sum", "ms_per_step": ms_f,
+               "value": nominal_path_steps(cfg) / (ms_f / 1e3), "price": est_f.price, "ci95": est_f.ci95}
     h2d, d2h = N.transfer_read()
     ms = float(np.mean(times))
     wall = float(np.mean(walls))
@@ -216,7 +237,10 @@ def run_engine(args, cfg):
     peak = FP64_LANES_PER_SM * N_SMS * sm_mhz * 1e6 / 1e12  # T fp64 lane-ops/s at the sampled clock
     if mode == "fast":
         peak *= 2.0  # fp32 lanes
-    achieved = (kern_steps * cfg["d"] * DP_OPS_PER_ASSET_STEP) / (kern_ms / 1e3) / 1e12 if kern_ms > 0 else 0.0
+    if mode == "parity":
+        achieved = (kern_steps * cfg["d"] * DP_OPS_PER_ASSET_STEP) / (kern_ms / 1e3) / 1e12 if kern_ms > 0 else 0.0
+    else:  # fast mode: no calibrated op model yet; report the rate, no fraction
+        achieved = None
     total_launches = sum(v[1] for v in prof.values())
     total_kernel_ms = sum(v[0] for v in prof.values())
 
@@ -241,10 +265,13 @@ def run_engine(args, cfg):
                     "note": "public API (numpy in/out) wall clock incl. host staging"},
             "gpu_launches": total_launches // max(args.steps, 1),
             "kernel_ms_per_step": {k: v[0] / max(args.steps, 1) for k, v in prof.items() if v[1]},
-            "roofline": {"bound": "fp64-pipe" if mode == "parity" else "fp32-pipe", "achieved": achieved,
-                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                         "traffic": None, "kernel": "walk_units+iz_probes",
-                         "work": f"{DP_OPS_PER_ASSET_STEP:g} modelled DP lane-ops x executed asset-steps "
+            "roofline": {"bound": "fp64-pipe" if mode == "parity" else "fp32/sfu-issue", "achieved": achieved,
+                         "peak": peak if mode == "parity" else None, "unit": "TFLOP/s",
+                         "frac": achieved / peak if achieved is not None else None,
+                         "asset_steps_per_s": kern_steps * cfg["d"] / (kern_ms / 1e3) if kern_ms > 0 else None,
+                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r01 capture)",
+                         "kernel": "walk_units+iz_probes",
+                         "work": f"{DP_OPS_PER_ASSET_STEP:g} fp64 lane-ops (ncu-measured) x executed asset-steps "
                                  f"({kern_steps // max(args.steps, 1)} path-steps x d per step)",
                          "kernel_ms_per_step": kern_ms / max(args.steps, 1),
                          "launches_per_step": kern_launches / max(args.steps, 1),
@@ -253,6 +280,8 @@ def run_engine(args, cfg):
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg)
+        if alt is not None:
+            line["fast_mode"] = alt
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -359,6 +388,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
     ap.add_argument("--mode", choices=("parity", "fast"), default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fast-line", action="store_true", help="skip the fast-mode companion measurement")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     line = run_reference(args, cfg) if args.impl == "reference" else run_engine(args, cfg)

@@ -14,9 +14,13 @@ p, s = bench.build_objects(cfg, E)
 rule, _ = E.build_cmc_rule(p, s, E.CmcBuildConfig(cfg["n_train"], cfg["n_label"], cfg["rounds"]), seed=1827, mode=mode)
 mp = pack_market(p, s)
 rp = rule.pack()
+from paper_0805_1827_b200 import _native as N
+N.profile_reset()
 t0 = time.perf_counter()
 G.cmc_calc(mp, rp, 1, 1827, 0, cfg["n_train"], cfg["n_label"], bridge_scalars(p, s, 1), mode=mode)
 t1 = time.perf_counter()
+s_lab = N.profile_read()["walk"][2]
 G.price_blocks(mp, rp, 1 << 22, 1827, mode=mode)
 t2 = time.perf_counter()
-print(f"labels(date1) {1e3*(t1-t0):.2f} ms  pricing(2^22) {1e3*(t2-t1):.2f} ms")
+s_all = N.profile_read()["walk"][2]
+print(f"labels(date1) {1e3*(t1-t0):.2f} ms  pricing(2^22) {1e3*(t2-t1):.2f} ms  path-steps: labels {s_lab} pricing {s_all - s_lab}")
