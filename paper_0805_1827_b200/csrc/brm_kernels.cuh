@@ -245,8 +245,9 @@ __global__ void __launch_bounds__(256) decisions(DecisionParams P) {
     R v[D > 0 ? D : kMaxD];
     #pragma unroll
     for (int a = 0; a < dim_of<D>(d); ++a) v[a] = (R)P.states[i * d + a];
-    const R pay = payoff<D>(M, v);
-    P.out[i] = (pay > (R)0 && rule_stop<D>(M, P.m, v)) ? 1 : 0;
+    R agg;
+    const R pay = payoff_agg<D>(M, v, agg);
+    P.out[i] = (pay > (R)0 && rule_stop<D>(M, P.m, v, agg)) ? 1 : 0;
   }
 }
 
