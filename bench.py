@@ -162,10 +162,13 @@ def run_engine(args, cfg):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # gloo: host-staged collectives (lets several ranks share one GPU in tests)
+            dist.init_process_group("gloo")
     import paper_0805_1827_b200 as E
     from paper_0805_1827_b200 import _native as N
 
@@ -389,8 +392,14 @@ def main():
     ap.add_argument("--mode", choices=("parity", "fast"), default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fast-line", action="store_true", help="skip the fast-mode companion measurement")
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
+    ap.add_argument("--scale", type=float, default=1.0, help="scale n_train / n_paths (tests only)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.scale != 1.0:
+        for key in ("n_train", "n_paths", "j_points"):
+            if key in cfg:
+                cfg[key] = max(1, int(cfg[key] * args.scale))
     line = run_reference(args, cfg) if args.impl == "reference" else run_engine(args, cfg)
     if line is not None:
         print(json.dumps(line), flush=True)
