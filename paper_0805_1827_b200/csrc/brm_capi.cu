@@ -953,8 +953,11 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   BRM_TRY(call.out(out_iterations, n, &P.out_iter));
   BRM_TRY(call.out(out_converged, n, &P.out_conv));
   // cluster size: enough CTAs per probe to give each lane a path or two
+  // cluster size: up to 8 CTAs per probe, fewer when the probes would not fit
+  // in one wave (2 walker CTAs per SM) or when there are too few inner paths
   int csize = 8;
   while (csize > 1 && (int64_t)csize * kWalkThreads / 2 > n_inner) csize >>= 1;
+  while (csize > 1 && n * csize > 2LL * c->info.sms) csize >>= 1;
   const int per_cta = (n_inner + csize - 1) / csize;
   P.vals_offset = smem_model(c);
   P.steps = step_counter(PK_IZ);

@@ -4,7 +4,7 @@
 (lowdisc.py:26-110: same multiplier table semantics, same mapping), so
 ``build_iz_boundary`` probes the reference's points.  ``uniform_log_grid``
 draws J points uniformly in the log-price box from the keyed Philox stream
-StreamKey(seed, GLP, j, 0) (BASELINE.json config 2: "64 boundary points per
+StreamKey(seed, GLP, 0, 0) (BASELINE.json config 2: "64 boundary points per
 date drawn uniformly in the reduced (d-1)-dim log-price box").
 """
 
@@ -84,15 +84,13 @@ def uniform_log_grid(j_points: int, dim: int, strike: float, seed: int, lo_mult:
                      hi_mult: float = 2.5) -> SeedGrid:
     """J points with log-prices uniform in [log(lo_mult K), log(hi_mult K)]^dim.
 
-    Uniforms are 53-bit words of StreamKey(seed, GLP, j, 0) from the device
-    generator; the returned box is the log box (clamp box of the log-space
-    boundary surface)."""
+    Uniforms are the 53-bit words j*dim .. j*dim+dim-1 of StreamKey(seed, GLP,
+    0, 0) from the device generator; the returned box is the log box (clamp box
+    of the log-space boundary surface)."""
     from . import backend
     lo, hi = math.log(lo_mult * strike), math.log(hi_mult * strike)
-    pts = np.empty((j_points, dim))
-    for j in range(j_points):
-        k, s = backend.derive_words(seed, 0, j, 0)
-        w = backend.raw_uint64(k, s, 0, dim)
-        u = ((w >> np.uint64(11)).astype(np.float64) + 0.5) * 2.0 ** -53
-        pts[j] = np.exp(lo + u * (hi - lo))
+    k, s = backend.derive_words(seed, 0, 0, 0)  # one GLP-phase stream for the whole grid
+    w = backend.raw_uint64(k, s, 0, j_points * dim).reshape(j_points, dim)
+    u = ((w >> np.uint64(11)).astype(np.float64) + 0.5) * 2.0 ** -53
+    pts = np.exp(lo + u * (hi - lo))
     return SeedGrid(points=pts, box=np.tile([lo, hi], (dim, 1)).astype(np.float64))
