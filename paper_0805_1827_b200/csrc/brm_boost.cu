@@ -152,6 +152,7 @@ struct BoostParams {
   int n, F, rounds;
   const double *xs;        // [n][F]
   const double *xsorted;   // [F][n]
+  const double *xt;        // [F][n] columns in sample order
   const double *y;         // [n] +-1
   double *w;               // [n] unnormalised weights of the current round
   double *wn;              // [F][n] per-CTA normalised copy (w / sum(w), numpy order)
@@ -165,9 +166,11 @@ struct BoostParams {
   const int2 *children;
   const int *level_end;
   int n_levels, root;
+  int tree_smem;           // 1: copy the tree tables into shared memory
   double *feat_err;        // [F]
   int *feat_pos;           // [F] 2*i + (pol == -1)
   double *wsub;            // [F][n] per-CTA scratch for the constant-stump sums
+  double *leafsum;         // [L] pairwise leaf sums of w (written by the reweighting CTAs)
   int *out_feat;
   double *out_thr, *out_pol, *out_alpha, *out_err;
   int *out_count;
@@ -176,51 +179,119 @@ struct BoostParams {
   long long *timing;  // optional per-phase clock64 totals of CTA 0 (diagnostics)
 };
 
-// CTA-wide numpy-order sum of a[0..n) (a divided by `div` on the fly when
-// div != 1); every thread gets the result.  s_node holds L + I doubles.
-__device__ double cta_pairwise(const BoostParams &P, const double *a, double *s_node) {
-  const int L = P.n_leaves;
-  // leaves: 8 lanes per leaf, lane j owns numpy's accumulator r[j] (elements
-  // j, j+8, ...); pair sums by shuffles are exact (IEEE addition commutes), the
-  // tail of len % 8 elements is added in order by the group's first lane
+// The recursion tree as the kernel reads it (shared-memory copy when it fits).
+struct PwView {
+  const int2 *leaves, *children;
+  const int *level_end;
+  int L, n_levels, root;
+};
+
+// numpy pairwise leaves [l_lo, l_hi) of a[0..n) into dst[l]: 8 lanes per
+// leaf, lane j owns numpy's accumulator r[j] (elements j, j+8, ...); pair sums
+// by shuffles are exact (IEEE addition commutes), the tail of len % 8 elements
+// is added in order (values gathered by shuffles).  op(i, a[i]) maps each
+// element to the value summed (loads only); sink(i, v) may then store it (the
+// normalise / reweight passes).  Keeping the stores out of op lets all loads
+// of a lane issue before the first store, which the compiler must otherwise
+// order behind it (the pointers may alias).
+struct PwNoSink {
+  __device__ __forceinline__ void operator()(int, double) const {}
+};
+
+template <class Op, class Sink = PwNoSink>
+__device__ __forceinline__ void pw_leaf_sums(const PwView &T, const double *a, int l_lo, int l_hi, double *dst,
+                                             Op op, Sink sink = PwNoSink{}) {
   const int lane = threadIdx.x & 31, grp = lane >> 3, j = lane & 7;
   const int groups = (blockDim.x >> 5) * 4;
-  for (int l0 = (threadIdx.x >> 5) * 4; l0 < L; l0 += groups) {
+  for (int l0 = l_lo + (threadIdx.x >> 5) * 4; l0 < l_hi; l0 += groups) {
     const int l = l0 + grp;
-    const bool ok = l < L;
-    const int off = ok ? P.leaves[l].x : 0, len = ok ? P.leaves[l].y : 0;
+    const bool ok = l < l_hi;
+    const int2 lf = ok ? T.leaves[l] : make_int2(0, 0);
+    const int off = lf.x, len = lf.y;
     const int main = len >= 8 ? len - (len % 8) : 0;
-    double r = main ? a[off + j] : 0.0;
-    // leaves hold <= 128 elements: all 15 further loads of this lane are issued up front
-    double col[kPwBlock / 8 - 1];
+    // leaves hold <= 128 elements: all 16 loads of this lane are issued up front
+    const int tail = len - main;  // < 8 elements added in order after the accumulators
+    double col[kPwBlock / 8];
 #pragma unroll
-    for (int q = 0; q < kPwBlock / 8 - 1; ++q) col[q] = 8 * (q + 1) < main ? a[off + 8 * (q + 1) + j] : 0.0;
+    for (int q = 0; q < kPwBlock / 8; ++q) col[q] = 8 * q < main ? a[off + 8 * q + j] : 0.0;
+    double tv = j < tail ? a[off + main + j] : 0.0;
+    // the 16 mapped values are independent: form them all before the
+    // dependent adds so their loads / divisions overlap
 #pragma unroll
-    for (int q = 0; q < kPwBlock / 8 - 1; ++q)
-      if (8 * (q + 1) < main) r = __dadd_rn(r, col[q]);
+    for (int q = 0; q < kPwBlock / 8; ++q)
+      if (8 * q < main) col[q] = op(off + 8 * q + j, col[q]);
+    if (j < tail) tv = op(off + main + j, tv);
+#pragma unroll
+    for (int q = 0; q < kPwBlock / 8; ++q)
+      if (8 * q < main) sink(off + 8 * q + j, col[q]);
+    if (j < tail) sink(off + main + j, tv);
+    double r = main ? col[0] : 0.0;
+#pragma unroll
+    for (int q = 1; q < kPwBlock / 8; ++q)
+      if (8 * q < main) r = __dadd_rn(r, col[q]);
     r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
     r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
     r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
-    if (ok && j == 0) {
-      double res = main ? r : 0.0;
-      for (int i = main; i < len; ++i) res = __dadd_rn(res, a[off + i]);
-      s_node[l] = res;
+    double res = main ? r : 0.0;
+#pragma unroll
+    for (int t = 0; t < 7; ++t) {
+      const double x = __shfl_sync(0xffffffffu, tv, (lane & ~7) + t);
+      if (t < tail) res = __dadd_rn(res, x);
     }
+    if (ok && j == 0) dst[l] = res;
   }
+}
+
+// Combine the leaf sums in s_node[0..L) up numpy's recursion tree; every
+// thread gets the root.
+__device__ __forceinline__ double pw_tree_sum(const PwView &T, double *s_node) {
+  const int L = T.L;
   __syncthreads();
   int lo = 0;
-  for (int h = 0; h < P.n_levels; ++h) {
-    const int hi = P.level_end[h];
+  for (int h = 0; h < T.n_levels; ++h) {
+    const int hi = T.level_end[h];
     for (int j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-      const int2 c = P.children[j];
+      const int2 c = T.children[j];
       s_node[L + j] = __dadd_rn(s_node[c.x], s_node[c.y]);
     }
     lo = hi;
     __syncthreads();
   }
-  const double r = s_node[P.root];
+  const double r = s_node[T.root];
   __syncthreads();
   return r;
+}
+
+struct PwIdentity {
+  __device__ __forceinline__ double operator()(int, double x) const { return x; }
+};
+
+// CTA-wide numpy-order sum of a[0..n); every thread gets the result.
+// s_node holds L + I doubles.
+__device__ double cta_pairwise(const PwView &T, const double *a, double *s_node) {
+  pw_leaf_sums(T, a, 0, T.L, s_node, PwIdentity{});
+  return pw_tree_sum(T, s_node);
+}
+
+// s[j] = w[idx[j]] for j < cnt (cnt <= kTile): all index loads of a thread
+// are issued before the dependent value loads.
+__device__ __forceinline__ void gather_tile(const double *__restrict__ w, const int *__restrict__ idx, int cnt,
+                                            double *__restrict__ s) {
+  constexpr int G = kTile / kBoostThreads;
+  int id[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int j = threadIdx.x + g * kBoostThreads;
+    id[g] = j < cnt ? __ldg(idx + j) : -1;
+  }
+  double v[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) v[g] = id[g] >= 0 ? w[id[g]] : 0.0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int j = threadIdx.x + g * kBoostThreads;
+    if (j < cnt) s[j] = v[g];
+  }
 }
 
 struct Cand {
@@ -232,29 +303,36 @@ __device__ __forceinline__ bool cand_less(const Cand &a, const Cand &b) {
   return a.err < b.err || (a.err == b.err && a.key < b.key);
 }
 
-// Sequential prefix sums out[k] = in[0] + ... + in[k] continuing from *acc
-// (one thread).  Loads are batched ahead of the dependent adds.
+// Sequential prefix sums out[k] = in[0] + ... + in[k] continuing from acc
+// (one thread).  Ping-pong over two register chunks: chunk A is summed while
+// chunk B's shared-memory loads are in flight, then the reverse, so no load
+// latency is exposed (tools/micro_cuda/chain.cu: 9.2 cycles/element vs 13.4
+// for the plain loop unrolled by 8).
 __device__ __forceinline__ void serial_chain(const double *__restrict__ in, double *__restrict__ out, int cnt,
                                              double &acc) {
-  constexpr int B = 8;
+  constexpr int C = 16;
   int k = 0;
-  double cur[B];
-  if (cnt >= B) {
+  double a[C], b[C];
+  if (cnt >= 2 * C) {
 #pragma unroll
-    for (int j = 0; j < B; ++j) cur[j] = in[j];
+    for (int j = 0; j < C; ++j) a[j] = in[j];
   }
-  for (; k + B <= cnt; k += B) {
-    double nxt[B];
-    const bool more = k + 2 * B <= cnt;
+  for (; k + 2 * C <= cnt; k += 2 * C) {
 #pragma unroll
-    for (int j = 0; j < B; ++j) nxt[j] = more ? in[k + B + j] : 0.0;
+    for (int j = 0; j < C; ++j) b[j] = in[k + C + j];
 #pragma unroll
-    for (int j = 0; j < B; ++j) {
-      acc = __dadd_rn(acc, cur[j]);
+    for (int j = 0; j < C; ++j) {
+      acc = __dadd_rn(acc, a[j]);
       out[k + j] = acc;
     }
+    const bool more = k + 4 * C <= cnt;
 #pragma unroll
-    for (int j = 0; j < B; ++j) cur[j] = nxt[j];
+    for (int j = 0; j < C; ++j) a[j] = more ? in[k + 2 * C + j] : 0.0;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      acc = __dadd_rn(acc, b[j]);
+      out[k + C + j] = acc;
+    }
   }
   for (; k < cnt; ++k) {
     acc = __dadd_rn(acc, in[k]);
@@ -270,6 +348,7 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
   double *s_in_n = s_in_p + kTile;
   double *s_out_p = s_in_n + kTile;
   double *s_out_n = s_out_p + kTile;
+  unsigned char *s_after = reinterpret_cast<unsigned char *>(s_out_n + kTile);
   __shared__ Cand s_cand[kBoostThreads / 32];
   __shared__ int s_stop;
   __shared__ double s_alpha, s_thr, s_pol, s_err;
@@ -277,19 +356,42 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
 
   const int n = P.n, F = P.F;
   const int f = blockIdx.x;
-  const int slice = (n + gridDim.x - 1) / gridDim.x;
-  const int w_lo = blockIdx.x * slice, w_hi = min(w_lo + slice, n);
+  // reweighting slices are whole pairwise leaves, so each CTA also publishes
+  // the leaf sums of the new weights and sum(w) needs only the tree combine
+  const int L = P.n_leaves;
+  PwView T{P.leaves, P.children, P.level_end, L, P.n_levels, P.root};
+  if (P.tree_smem) {  // tree tables after the tiles: leaves, children, level ends
+    int2 *s_leaves = reinterpret_cast<int2 *>(s_after);
+    int2 *s_children = s_leaves + L;
+    int *s_level = reinterpret_cast<int *>(s_children + max(L - 1, 0));
+    for (int i = threadIdx.x; i < L; i += blockDim.x) s_leaves[i] = P.leaves[i];
+    for (int i = threadIdx.x; i < L - 1; i += blockDim.x) s_children[i] = P.children[i];
+    for (int i = threadIdx.x; i < P.n_levels; i += blockDim.x) s_level[i] = P.level_end[i];
+    T.leaves = s_leaves;
+    T.children = s_children;
+    T.level_end = s_level;
+    __syncthreads();
+  }
+  const int l_lo = (int)((long long)blockIdx.x * L / gridDim.x), l_hi = (int)((long long)(blockIdx.x + 1) * L / gridDim.x);
   double *wn = P.wn + (size_t)f * n;
   int count = 0;
   long long t_mark = 0;
 
   for (int round = 0; round < P.rounds; ++round) {
     if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) t_mark = clock64();
-    // ---- w / w.sum() (numpy pairwise order), CTA-private copy ------------
-    const double s = round == 0 ? 1.0 : cta_pairwise(P, P.w, s_node);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) wn[i] = round == 0 ? P.w[i] : div_nb(P.w[i], s);
-    __syncthreads();
-    const double total = cta_pairwise(P, wn, s_node);
+    // ---- wn = w / w.sum() (numpy pairwise order), CTA-private copy, and
+    // total = wn.sum() in the same pass ----------------------------------
+    double total;
+    if (round == 0) {
+      pw_leaf_sums(T, P.w, 0, L, s_node, PwIdentity{}, [&](int i, double v) { wn[i] = v; });
+      total = pw_tree_sum(T, s_node);
+    } else {
+      for (int l = threadIdx.x; l < L; l += blockDim.x) s_node[l] = __ldcg(P.leafsum + l);
+      const double s = pw_tree_sum(T, s_node);
+      pw_leaf_sums(
+          T, P.w, 0, L, s_node, [&](int, double x) { return div_nb(x, s); }, [&](int i, double v) { wn[i] = v; });
+      total = pw_tree_sum(T, s_node);
+    }
     if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[1] += now - t_mark; t_mark = now; }
     // ---- split search on feature f -------------------------------------
     if (f < F) {
@@ -304,10 +406,14 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
       const int chain_p = blockDim.x - 64, chain_n = blockDim.x - 32;
       for (int t0 = 0; t0 < max(n_pos, n_neg); t0 += kTile) {
         const int tp = max(0, min(kTile, n_pos - t0)), tn = max(0, min(kTile, n_neg - t0));
-        for (int j = threadIdx.x; j < tp; j += blockDim.x) s_in_p[j] = wn[pid[t0 + j]];
-        for (int j = threadIdx.x; j < tn; j += blockDim.x) s_in_n[j] = wn[nid[t0 + j]];
+        gather_tile(wn, pid + t0, tp, s_in_p);
+        gather_tile(wn, nid + t0, tn, s_in_n);
         __syncthreads();
-        if (threadIdx.x == chain_p) serial_chain(s_in_p, s_out_p, tp, pacc);
+        if (threadIdx.x == chain_p) {
+          const long long c0 = P.timing ? clock64() : 0;
+          serial_chain(s_in_p, s_out_p, tp, pacc);
+          if (P.timing && blockIdx.x == 0) P.timing[7] += clock64() - c0;
+        }
         else if (threadIdx.x == chain_n) serial_chain(s_in_n, s_out_n, tn, nacc);
         __syncthreads();
         for (int j = threadIdx.x; j < tp; j += blockDim.x) pc[t0 + j] = s_out_p[j];
@@ -320,7 +426,7 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
       const int2 *brk = P.brk + (size_t)f * n;
       const double tot_neg = n_neg > 0 ? nc[n_neg - 1] : 0.0;
       Cand best{__longlong_as_double(0x7ff0000000000000LL), 0x7fffffff};
-      constexpr int U = 8;
+      constexpr int U = 16;
       for (int i0 = threadIdx.x; i0 < n - 1; i0 += U * blockDim.x) {
         int2 bi[U];
         double pcs[U], ncs[U];
@@ -365,15 +471,33 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
     grid.sync();
     if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[4] += now - t_mark; t_mark = now; }
     // ---- pick the winner (every CTA, same answer) ------------------------
-    if (threadIdx.x == 0) {
-      double be = __longlong_as_double(0x7ff0000000000000LL);
-      int bf = -1, bk = 0;
-      for (int g = 0; g < F; ++g)
-        if (P.feat_pos[g] != 0x7fffffff && P.feat_err[g] < be) {
-          be = P.feat_err[g];
+    // first minimum over features in order: (err, feature) lexicographic
+    double be = __longlong_as_double(0x7ff0000000000000LL);
+    int bf = 0x7fffffff, bk = 0;
+    if (threadIdx.x < 32) {
+      for (int g = threadIdx.x; g < F; g += 32) {
+        const int pos = __ldcg(P.feat_pos + g);
+        const double e = __ldcg(P.feat_err + g);
+        if (pos != 0x7fffffff && e < be) {
+          be = e;
           bf = g;
-          bk = P.feat_pos[g];
+          bk = pos;
         }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double oe = __shfl_down_sync(0xffffffffu, be, off);
+        const int of = __shfl_down_sync(0xffffffffu, bf, off);
+        const int ok = __shfl_down_sync(0xffffffffu, bk, off);
+        if (oe < be || (oe == be && of < bf)) {
+          be = oe;
+          bf = of;
+          bk = ok;
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      if (bf == 0x7fffffff) bf = -1;
       if (bf < 0) {
         s_stop = 2;  // every feature constant: resolved below by the whole CTA
         s_feat = 0;
@@ -395,7 +519,7 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
       double *ws = P.wsub + (size_t)blockIdx.x * n;
       for (int i = threadIdx.x; i < n; i += blockDim.x) ws[i] = __dmul_rn(wn[i], P.y[i]);
       __syncthreads();
-      const double swy = cta_pairwise(P, ws, s_node);
+      const double swy = cta_pairwise(T, ws, s_node);
       const double pol = swy >= 0.0 ? 1.0 : -1.0;
       if (threadIdx.x == 0) {
         int k = 0;
@@ -444,11 +568,15 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
       const double a = s_alpha, thr = s_thr, pol = s_pol;
       const int feat = s_feat;
       const double e_agree = exp(-a), e_miss = exp(a);
-      for (int i = w_lo + threadIdx.x; i < w_hi; i += blockDim.x) {
-        const double pred = P.xs[(size_t)i * F + feat] > thr ? pol : -pol;
-        P.w[i] = __dmul_rn(wn[i], (P.y[i] * pred > 0.0) ? e_agree : e_miss);
-      }
+      pw_leaf_sums(
+          T, wn, l_lo, l_hi, P.leafsum,
+          [&](int i, double x) {
+            const double pred = __ldg(P.xt + (size_t)feat * n + i) > thr ? pol : -pol;
+            return __dmul_rn(x, (__ldg(P.y + i) * pred > 0.0) ? e_agree : e_miss);
+          },
+          [&](int i, double v) { P.w[i] = v; });
     }
+    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) P.timing[0] += clock64() - t_mark;
     grid.sync();
     if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[6] += now - t_mark; t_mark = now; }
   }
@@ -861,6 +989,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
+  retain_pool(device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   {
     Scratch S(s);
@@ -947,6 +1076,8 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
     BCU(S.get(&d_rerr, rounds));
     BCU(S.get(&d_count, 1));
     root = pw_tree(n, tree);
+    double *d_leafsum;
+    BCU(S.get(&d_leafsum, tree.leaves.size()));
     BCU(S.get(&d_leaves, tree.leaves.size()));
     BCU(cudaMemcpyAsync(d_leaves, tree.leaves.data(), sizeof(int2) * tree.leaves.size(), cudaMemcpyHostToDevice, s));
     BCU(S.get(&d_children, tree.children.size()));
@@ -966,6 +1097,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       P.n_pos = npos;
       P.xs = d_xs;
       P.xsorted = d_xsorted;
+      P.xt = d_xt;
       P.y = d_y;
       P.w = d_w;
       P.wn = d_wn;
@@ -984,6 +1116,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       P.feat_err = d_err;
       P.feat_pos = d_pos;
       P.wsub = d_wsub;
+      P.leafsum = d_leafsum;
       P.out_feat = d_feat;
       P.out_thr = d_thr;
       P.out_pol = d_pol;
@@ -997,8 +1130,16 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
         BCU(cudaMemsetAsync(d_timing, 0, 8 * sizeof(long long), s));
       }
       P.timing = d_timing;
-      const size_t smem = sizeof(double) * (2 * tree.leaves.size() + 4 * kTile);
-      BCU(cudaFuncSetAttribute(boost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int smem_max = 0;
+      BCU(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+      const size_t smem_cap = (size_t)smem_max - 2048;  // static shared arrays of the kernel
+      const size_t tree_bytes = sizeof(int2) * (tree.leaves.size() + tree.children.size()) +
+                                sizeof(int) * tree.level_end.size();
+      size_t smem = sizeof(double) * (2 * tree.leaves.size() + 4 * kTile);
+      P.tree_smem = smem + tree_bytes <= smem_cap ? 1 : 0;
+      if (P.tree_smem) smem += tree_bytes;
+      void *boost_fn = (void *)boost_kernel;
+      BCU(cudaFuncSetAttribute(boost_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       void *args[] = {&P};
       const int tok = prof_begin(PK_BOOST, s);
       if (mode == BRM_MODE_FAST) {
@@ -1025,15 +1166,16 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
         void *qargs[] = {&Q};
         BCU(cudaLaunchCooperativeKernel((void *)boost_fast_kernel, dim3(F), dim3(kBoostThreads), qargs, 0, s));
       } else {
-        BCU(cudaLaunchCooperativeKernel((void *)boost_kernel, dim3(F), dim3(kBoostThreads), args, smem, s));
+        BCU(cudaLaunchCooperativeKernel(boost_fn, dim3(F), dim3(kBoostThreads), args, smem, s));
       }
       prof_end(tok, s);
       if (timing) {
         long long h[8];
         BCU(cudaMemcpyAsync(h, d_timing, sizeof h, cudaMemcpyDeviceToHost, s));
         BCU(cudaStreamSynchronize(s));
-        fprintf(stderr, "boost phases (kcycles, CTA 0): norm+total %.0f chains %.0f scan %.0f sync1 %.0f pick %.0f reweight+sync2 %.0f\n",
-                h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, h[6] / 1e3);
+        fprintf(stderr, "boost phases (kcycles, CTA 0): norm+total %.0f chains %.0f (positive chain alone %.0f) scan %.0f "
+                "sync1 %.0f pick %.0f reweight+sync2 %.0f (reweight alone %.0f)\n",
+                h[1] / 1e3, h[2] / 1e3, h[7] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, h[6] / 1e3, h[0] / 1e3);
       }
     }
     BCU(cudaGetLastError());
@@ -1073,6 +1215,7 @@ extern "C" int brm_lstsq(int32_t device, void *stream, const double *design, con
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
+  retain_pool(device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double *d_design = nullptr, *d_levels = nullptr, *d_coeffs = nullptr;
   int *d_cols = nullptr, *d_rank = nullptr;

@@ -175,11 +175,31 @@ int fetch(const T *src, size_t count, std::vector<T> &dst, const char *name) {
 
 int quad_basis_size(int k) { return 1 + k + k * (k + 1) / 2; }
 
+}  // namespace
+
+void brm::retain_pool(int dev) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return;
+  done[dev] = true;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+}
+
+namespace {
+
 // Library stream of a device (created once, non-blocking, never destroyed).
 cudaStream_t device_stream(int dev) {
   static std::mutex mu;
   static cudaStream_t streams[64] = {};
   if (dev < 0 || dev >= 64) return nullptr;
+  retain_pool(dev);
   std::lock_guard<std::mutex> lk(mu);
   if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
     cudaGetLastError();

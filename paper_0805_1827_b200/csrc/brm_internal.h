@@ -104,5 +104,9 @@ void *sample_kernel();
 void *fill_raw_kernel();
 void *fill_normals_kernel();
 void *math_selftest_kernel();
+// Keep freed stream-ordered allocations in the device's default pool across
+// synchronisations (the pool's default release threshold of 0 hands them back
+// to the driver at every sync, and the next call re-maps them).
+void retain_pool(int dev);
 
 }  // namespace brm

@@ -103,8 +103,106 @@ __device__ void int_chain(const double *__restrict__ in, double *__restrict__ ou
   acc = s;
 }
 
+// the kernel's serial_chain (loads batched 8 ahead)
+__device__ __forceinline__ void batched_chain(const double *__restrict__ in, double *__restrict__ out, int cnt,
+                                             double &acc) {
+  constexpr int B = 8;
+  int k = 0;
+  double cur[B];
+  if (cnt >= B) {
+#pragma unroll
+    for (int j = 0; j < B; ++j) cur[j] = in[j];
+  }
+  for (; k + B <= cnt; k += B) {
+    double nxt[B];
+    const bool more = k + 2 * B <= cnt;
+#pragma unroll
+    for (int j = 0; j < B; ++j) nxt[j] = more ? in[k + B + j] : 0.0;
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      acc = __dadd_rn(acc, cur[j]);
+      out[k + j] = acc;
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) cur[j] = nxt[j];
+  }
+  for (; k < cnt; ++k) {
+    acc = __dadd_rn(acc, in[k]);
+    out[k] = acc;
+  }
+}
+
 // both read from / write to shared memory, as in the AdaBoost kernel (tiles of 4096)
 constexpr int T = 4096;
+template <int U>
+__device__ __forceinline__ void unrolled_chain(const double *__restrict__ in, double *__restrict__ out, int cnt,
+                                               double &acc) {
+#pragma unroll U
+  for (int k = 0; k < cnt; ++k) {
+    acc = __dadd_rn(acc, in[k]);
+    out[k] = acc;
+  }
+}
+
+// ping-pong: chunk A summed while chunk B loads, then the reverse (no moves)
+template <int C>
+__device__ __forceinline__ void pingpong_chain(const double *__restrict__ in, double *__restrict__ out, int cnt,
+                                               double &acc) {
+  int k = 0;
+  double a[C], b[C];
+  if (cnt >= 2 * C) {
+#pragma unroll
+    for (int j = 0; j < C; ++j) a[j] = in[j];
+  }
+  for (; k + 2 * C <= cnt; k += 2 * C) {
+#pragma unroll
+    for (int j = 0; j < C; ++j) b[j] = in[k + C + j];
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      acc = __dadd_rn(acc, a[j]);
+      out[k + j] = acc;
+    }
+    const bool more = k + 4 * C <= cnt;
+#pragma unroll
+    for (int j = 0; j < C; ++j) a[j] = more ? in[k + 2 * C + j] : 0.0;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      acc = __dadd_rn(acc, b[j]);
+      out[k + C + j] = acc;
+    }
+  }
+  for (; k < cnt; ++k) {
+    acc = __dadd_rn(acc, in[k]);
+    out[k] = acc;
+  }
+}
+
+template <int V>
+__global__ void run_var(const double *in, double *out, int n, long long *cyc) {
+  extern __shared__ double sm[];
+  double *si = sm, *so = sm + T;
+  double acc = 0.0;
+  long long tot = 0;
+  for (int t0 = 0; t0 < n; t0 += T) {
+    const int tn = min(T, n - t0);
+    for (int j = threadIdx.x; j < tn; j += blockDim.x) si[j] = in[t0 + j];
+    __syncthreads();
+    long long a = clock64();
+    if (threadIdx.x == blockDim.x - 32) {
+      if (V == 0) unrolled_chain<8>(si, so, tn, acc);
+      if (V == 1) unrolled_chain<16>(si, so, tn, acc);
+      if (V == 2) unrolled_chain<32>(si, so, tn, acc);
+      if (V == 3) pingpong_chain<8>(si, so, tn, acc);
+      if (V == 4) pingpong_chain<16>(si, so, tn, acc);
+    }
+    tot += clock64() - a;
+    __syncthreads();
+    for (int j = threadIdx.x; j < tn; j += blockDim.x) out[t0 + j] = so[j];
+    __syncthreads();
+  }
+  if (threadIdx.x == blockDim.x - 32) *cyc = tot;
+}
+
 __global__ void run_seq(const double *in, double *out, int n, long long *cyc) {
   extern __shared__ double sm[];
   double *si = sm, *so = sm + T;
@@ -124,6 +222,26 @@ __global__ void run_seq(const double *in, double *out, int n, long long *cyc) {
   if (threadIdx.x == 0) *cyc = tot;
 }
 
+template <int WARPS>
+__global__ void run_batched(const double *in, double *out, int n, long long *cyc) {
+  extern __shared__ double sm[];
+  double *si = sm, *so = sm + T;
+  double acc = 0.0;
+  long long tot = 0;
+  for (int t0 = 0; t0 < n; t0 += T) {
+    const int tn = min(T, n - t0);
+    for (int j = threadIdx.x; j < tn; j += blockDim.x) si[j] = in[t0 + j];
+    __syncthreads();
+    long long a = clock64();
+    if (threadIdx.x == blockDim.x - 32) batched_chain(si, so, tn, acc);
+    tot += clock64() - a;
+    __syncthreads();
+    for (int j = threadIdx.x; j < tn; j += blockDim.x) out[t0 + j] = so[j];
+    __syncthreads();
+  }
+  if (threadIdx.x == blockDim.x - 32) *cyc = tot;
+}
+
 __global__ void run_warp(const double *in, double *out, int n, long long *cyc, int *passes) {
   extern __shared__ double sm[];
   double *si = sm, *so = sm + T;
@@ -141,6 +259,18 @@ __global__ void run_warp(const double *in, double *out, int n, long long *cyc, i
     __syncthreads();
   }
   if (threadIdx.x == 0) *cyc = tot;
+}
+
+static double r1ref(const std::vector<double> &h, int i) {  // sequential prefix, cached
+  static std::vector<double> c;
+  static const double *key = nullptr;
+  if (key != h.data() || c.size() != h.size()) {
+    key = h.data();
+    c.resize(h.size());
+    double s = 0.0;
+    for (size_t j = 0; j < h.size(); ++j) c[j] = (s += h[j]);
+  }
+  return c[i];
 }
 
 int main() {
@@ -167,6 +297,33 @@ int main() {
     cudaFuncSetAttribute(run_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * T * 8);
     run_seq<<<1, 32, 2 * T * 8>>>(din, o1, n, cyc);
     cudaMemcpy(&c1, cyc, 8, cudaMemcpyDeviceToHost);
+    {
+      long long cb1, cb8;
+      cudaFuncSetAttribute(run_batched<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * T * 8);
+      cudaFuncSetAttribute(run_batched<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * T * 8);
+      run_batched<1><<<1, 32, 2 * T * 8>>>(din, o2, n, cyc + 1);
+      cudaMemcpy(&cb1, cyc + 1, 8, cudaMemcpyDeviceToHost);
+      run_batched<8><<<1, 256, 2 * T * 8>>>(din, o2, n, cyc + 1);
+      cudaMemcpy(&cb8, cyc + 1, 8, cudaMemcpyDeviceToHost);
+      printf("  batched chain: 1 warp %.1f cyc/elem, 8 warps (chain on warp 7) %.1f cyc/elem\n", (double)cb1 / n,
+             (double)cb8 / n);
+    }
+    {
+      const char *names[] = {"unroll8", "unroll16", "unroll32", "pingpong8", "pingpong16"};
+      void (*ks[])(const double *, double *, int, long long *) = {run_var<0>, run_var<1>, run_var<2>, run_var<3>,
+                                                                  run_var<4>};
+      for (int v = 0; v < 5; ++v) {
+        long long cv;
+        cudaFuncSetAttribute(ks[v], cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * T * 8);
+        ks[v]<<<1, 256, 2 * T * 8>>>(din, o2, n, cyc + 1);
+        cudaMemcpy(&cv, cyc + 1, 8, cudaMemcpyDeviceToHost);
+        std::vector<double> rv(n);
+        cudaMemcpy(rv.data(), o2, 8 * n, cudaMemcpyDeviceToHost);
+        int bad = 0;
+        for (int i = 0; i < n; ++i) bad += rv[i] != r1ref(h, i);
+        printf("  %s: %.1f cyc/elem (mismatches %d)\n", names[v], (double)cv / n, bad);
+      }
+    }
     run_warp<<<1, 32, 2 * T * 8>>>(din, o2, n, cyc + 1, passes);
     cudaMemcpy(&c2, cyc + 1, 8, cudaMemcpyDeviceToHost);
     cudaMemcpy(&np, passes, 4, cudaMemcpyDeviceToHost);
