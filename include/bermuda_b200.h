@@ -41,7 +41,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define BRM_ABI_VERSION 1
+#define BRM_ABI_VERSION 2
 
 enum brm_status {
     BRM_OK = 0,
@@ -103,6 +103,20 @@ int brm_device_count(int32_t *count);
 int brm_ctx_create(const brm_market_desc *market, const brm_rule_desc *rule, int32_t device, int32_t mode,
                    brm_ctx **out);
 int brm_ctx_destroy(brm_ctx *ctx);
+/* Device-resident backward induction (the date loop of build_cmc_rule,
+ * boundary_cmc.py:248-278, without a host round trip per date): a CMC
+ * context whose dates start empty (intercept -1, never exercise) with room
+ * for `capacity` stumps per date (<= 1024).  brm_ctx_set_ensemble writes
+ * date `date`'s ensemble -- arrays sized [capacity], *count stumps used,
+ * *intercept -- into the image on the context's stream (inputs may be
+ * device pointers, e.g. the outputs of brm_fit_ensemble with
+ * BRM_FIT_DEVICE_RESULT), building the date's step tables on the device.
+ * The image equals the one brm_ctx_create builds for the same ensembles
+ * (RulePack.from_stumps, packs.py:149-182) up to the layout. */
+int brm_ctx_create_cmc(const brm_market_desc *market, int32_t call_like, int32_t capacity, int32_t device,
+                       int32_t mode, brm_ctx **out);
+int brm_ctx_set_ensemble(brm_ctx *ctx, int32_t date, const int32_t *feat, const double *thr, const double *pol,
+                         const double *alpha, const int32_t *count, const double *intercept);
 /* Launch on a caller-owned cudaStream_t (e.g. torch's current stream); NULL restores the context's own. */
 int brm_ctx_set_stream(brm_ctx *ctx, void *cuda_stream);
 /* Fixed-input mode: draw index i of every stream reads normals[i - base]
@@ -190,8 +204,13 @@ int brm_cmc_calc(brm_ctx *ctx, int32_t sampler, int32_t m, uint64_t seed, int64_
  * rules.  flags BRM_FIT_SINGLE_STUMP: one fit_stump search (boosting.py:
  * 126-171) with the given weights, no boosting rules.  Outputs sized
  * [rounds]; *out_count stumps picked; out_err the weighted error of each;
- * *out_intercept the ensemble intercept.  stream: cudaStream_t or NULL. */
+ * *out_intercept the ensemble intercept.  stream: cudaStream_t or NULL.
+ * flags BRM_FIT_DEVICE_RESULT: every output (count and intercept included)
+ * is a device pointer, the stump arrays are written in full ([rounds],
+ * entries past *out_count unspecified) and the call returns without
+ * synchronising: results are ordered on `stream`. */
 #define BRM_FIT_SINGLE_STUMP 1
+#define BRM_FIT_DEVICE_RESULT 2
 int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, void *stream, const double *xs,
                      const double *betas, const double *weights, int64_t n, int32_t F, int32_t rounds,
                      int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha, double *out_err,

@@ -19,6 +19,8 @@ _LIB_PATH = Path(os.environ.get("BRM_LIB_PATH") or Path(__file__).resolve().pare
 BRM_OK, BRM_EINVAL, BRM_ENOMEM, BRM_ECUDA, BRM_ENODEV = range(5)
 MODE_PARITY, MODE_FAST = 0, 1
 FIT_SINGLE_STUMP = 1
+FIT_DEVICE_RESULT = 2
+ABI_VERSION = 2
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -49,6 +51,10 @@ _SIGNATURES = {
     "brm_ctx_create": (C.c_int, [C.POINTER(MarketDesc), C.POINTER(RuleDesc), C.c_int32, C.c_int32,
                                  C.POINTER(C.c_void_p)]),
     "brm_ctx_destroy": (C.c_int, [C.c_void_p]),
+    "brm_ctx_create_cmc": (C.c_int, [C.POINTER(MarketDesc), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                     C.POINTER(C.c_void_p)]),
+    "brm_ctx_set_ensemble": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p]),
     "brm_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "brm_ctx_supply_normals": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64]),
     "brm_derive_words": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, _up, _up]),
@@ -73,7 +79,7 @@ _SIGNATURES = {
                                C.c_void_p, C.c_void_p, C.c_void_p]),
     "brm_fit_ensemble": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
-                                   C.c_void_p, C.c_void_p, _ip, _dp]),
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "brm_profile_enable": (C.c_int, [C.c_int32]),
     "brm_profile_reset": (C.c_int, []),
     "brm_profile_read": (C.c_int, [C.c_int32, _dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
@@ -93,7 +99,7 @@ def _load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.brm_abi_version() != 1:
+    if lib.brm_abi_version() != ABI_VERSION:
         raise ImportError("libbermuda_b200.so ABI version mismatch")
     return lib
 

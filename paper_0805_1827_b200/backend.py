@@ -87,9 +87,9 @@ def path_values(mp, rp, start_values, m_start: int, n_paths: int, key64, stream6
     return vals, stops
 
 
-def decisions(mp, rp, states, m: int, mode=None, device=None) -> np.ndarray:
+def decisions(mp, rp, states, m: int, mode=None, device=None, ctx=None) -> np.ndarray:
     """Exercise decisions of the rule for states[n, d] at date m (pricer.py:104-133)."""
-    ctx = get_context(mp, rp, device, mode)
+    ctx = get_context(mp, rp, device, mode) if ctx is None else ctx
     st = N.f64(states).reshape(-1, int(mp.d))
     out = np.empty(st.shape[0], dtype=np.int32)
     N.check(N.lib.brm_decisions(ctx.handle, N.ptr(st), st.shape[0], int(m), N.ptr(out)))
@@ -200,10 +200,22 @@ def fit_ensemble_arrays(xs, betas, rounds: int, mode=None, device=None, weights=
     count, icept = C.c_int32(), C.c_double()
     N.check(N.lib.brm_fit_ensemble(_dev(device), resolve_mode(mode), N.FIT_SINGLE_STUMP if single else 0,
                                    N.stream_handle(stream), N.ptr(xs), N.ptr(betas), N.ptr(w), n, F, r,
-                                   N.ptr(feat), N.ptr(thr), N.ptr(pol), N.ptr(alpha), N.ptr(err), C.byref(count),
-                                   C.byref(icept)))
+                                   N.ptr(feat), N.ptr(thr), N.ptr(pol), N.ptr(alpha), N.ptr(err),
+                                   C.addressof(count), C.addressof(icept)))
     c = count.value
     return feat[:c], thr[:c], pol[:c], alpha[:c], err[:c], float(icept.value)
+
+
+def fit_ensemble_device(xs, betas, rounds: int, out, mode=None, device=None, stream=None) -> None:
+    """Device AdaBoost with device-resident results and no host synchronisation
+    (BRM_FIT_DEVICE_RESULT): ``out`` holds device tensors feat[int32, rounds],
+    thr/pol/alpha/err[f64, rounds], count[int32, 1], intercept[f64, 1]."""
+    from .context import resolve_mode
+    n, F = int(xs.shape[0]), int(xs.shape[1])
+    N.check(N.lib.brm_fit_ensemble(_dev(device), resolve_mode(mode), N.FIT_DEVICE_RESULT, N.stream_handle(stream),
+                                   N.ptr(xs), N.ptr(betas), None, n, F, int(rounds), N.ptr(out["feat"]),
+                                   N.ptr(out["thr"]), N.ptr(out["pol"]), N.ptr(out["alpha"]), N.ptr(out["err"]),
+                                   N.ptr(out["count"]), N.ptr(out["intercept"])))
 
 
 def lstsq(design, levels, k_coords: int, device=None, stream=None):
@@ -219,9 +231,10 @@ def lstsq(design, levels, k_coords: int, device=None, stream=None):
 
 
 def cmc_calc(mp, rp, m: int, seed: int, item_lo: int, n: int, n_label: int, bridge=None, sampler: str = "bridge",
-             out_features=None, out_beta=None, mode=None, device=None):
-    """Sample, featurise and label training points [item_lo, item_lo+n) of date m on the device."""
-    ctx = get_context(mp, rp, device, mode)
+             out_features=None, out_beta=None, mode=None, device=None, ctx=None):
+    """Sample, featurise and label training points [item_lo, item_lo+n) of date m on the device
+    (under ``ctx``'s rule when given, else the context of (mp, rp))."""
+    ctx = get_context(mp, rp, device, mode) if ctx is None else ctx
     d = int(mp.d)
     F = d + 1 if d > 1 else 1
     if out_features is None:

@@ -174,9 +174,84 @@ def _torch_cuda():
         return None
 
 
+# Largest slotted rule image (shared memory of every walker CTA) for which the
+# device-resident date loop is used; beyond it the per-date host-built images
+# are smaller and keep the walker's occupancy.
+_SLOT_IMAGE_LIMIT = 96 * 1024
+
+
+def slot_image_bytes(n_dates: int, capacity: int, n_features: int, fast: bool) -> int:
+    """Shared-memory bytes of a brm_ctx_create_cmc image (brm_internal.h SlotDims)."""
+    per_date_dbl = 2 * capacity + 2 * capacity + capacity + n_features  # thr, ap, thresholds, table values
+    n_dbl = (n_dates + 1) * per_date_dbl + 64
+    n_int = (n_dates + 1) * (capacity + 3 * n_features + 2)
+    return (4 if fast else 8) * n_dbl + 4 * n_int
+
+
+def _build_device_loop(params, spec, cfg, seed, sampler, mode, shard, torch, stream, mp, F, call_like):
+    """The backward date loop with every date's work enqueued on one stream and
+    no host round trip until the end: the fitted stumps stay in HBM and
+    brm_ctx_set_ensemble writes them into the rule image the next (earlier)
+    date labels under.  Per-date times are CUDA-event times."""
+    from .context import Context
+    nd, R = spec.n_dates, cfg.boost_rounds
+    ctx = Context.cmc_slots(mp, call_like, R, mode=mode)
+    ctx.set_stream(stream)
+    f64, i32 = torch.float64, torch.int32
+    out = {"feat": torch.zeros((nd + 1, R), dtype=i32, device="cuda"),
+           "thr": torch.zeros((nd + 1, R), dtype=f64, device="cuda"),
+           "pol": torch.zeros((nd + 1, R), dtype=f64, device="cuda"),
+           "alpha": torch.zeros((nd + 1, R), dtype=f64, device="cuda"),
+           "err": torch.zeros((nd + 1, R), dtype=f64, device="cuda"),
+           "count": torch.zeros((nd + 1,), dtype=i32, device="cuda"),
+           "intercept": torch.full((nd + 1,), -1.0, dtype=f64, device="cuda")}
+    pos = torch.zeros((nd + 1,), dtype=f64, device="cuda")
+    marks = []
+    for m in range(nd - 1, 0, -1):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        lo, hi = shard.range(cfg.n_train)
+        feats = torch.empty((hi - lo, F), dtype=f64, device="cuda")
+        betas = torch.empty((hi - lo,), dtype=f64, device="cuda")
+        if hi > lo:
+            _be.cmc_calc(mp, None, m, seed, lo, hi - lo, cfg.n_label, bridge_scalars(params, spec, m), sampler,
+                         feats, betas, mode=mode, ctx=ctx)
+        feats = shard.all_gather_rows(feats, cfg.n_train)
+        betas = shard.all_gather_rows(betas, cfg.n_train)
+        ev[1].record(stream)
+        date_out = {k: (v[m] if v.dim() == 2 else v[m:m + 1]) for k, v in out.items()}
+        _be.fit_ensemble_device(feats, betas, R, date_out, mode=mode, stream=stream)
+        ctx.set_ensemble(m, date_out["feat"], date_out["thr"], date_out["pol"], date_out["alpha"],
+                         date_out["count"], date_out["intercept"])
+        ev[2].record(stream)
+        pos[m] = (betas > 0).to(f64).mean()
+        marks.append((m, ev))
+    host = {k: v.cpu().numpy() for k, v in out.items()}  # the build's one synchronisation
+    pos_h = pos.cpu().numpy()
+    ensembles, report = {}, CmcBuildReport()
+    for m, ev in marks:
+        c = int(host["count"][m])
+        ens = ensemble_from_arrays(F, host["feat"][m, :c], host["thr"][m, :c], host["pol"][m, :c],
+                                   host["alpha"][m, :c], float(host["intercept"][m]))
+        ensembles[m] = ens
+        if not ens.rounds:
+            report.one_class_dates.append(m)
+        calc_s, class_s = ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3
+        report.calc_seconds += calc_s
+        report.class_seconds += class_s
+        report.per_date.append({"date_index": m, "calc_seconds": calc_s, "class_seconds": class_s,
+                                "positive_fraction": float(pos_h[m]), "rounds": len(ens.rounds)})
+    report.per_date.reverse()
+    return CmcRule(params.d, nd, call_like, ensembles), report
+
+
 def build_cmc_rule(params, spec, cfg: CmcBuildConfig, seed: int = 0, engine=None, backend=None, *,
-                   sampler: str = "bridge", mode=None) -> tuple[CmcRule, CmcBuildReport]:
-    """Fit the per-date classifiers by backward induction (boundary_cmc.py:230-281)."""
+                   sampler: str = "bridge", mode=None, device_loop=None) -> tuple[CmcRule, CmcBuildReport]:
+    """Fit the per-date classifiers by backward induction (boundary_cmc.py:230-281).
+
+    device_loop: enqueue every date without host round trips (default: on a
+    GPU when the slotted rule image fits, see ``slot_image_bytes``); False
+    rebuilds the rule image on the host per date.  Both give the same rule."""
     spec.validate_against(params)
     if sampler not in ("bridge", "forward"):
         raise ValueError(f"unknown sampler {sampler!r}")
@@ -189,6 +264,15 @@ def build_cmc_rule(params, spec, cfg: CmcBuildConfig, seed: int = 0, engine=None
     report = CmcBuildReport()
     torch = _torch_cuda()
     stream = torch.cuda.current_stream() if torch is not None else None
+    if device_loop is None:
+        from .context import resolve_mode
+        fast = resolve_mode(mode) == 1
+        device_loop = (torch is not None and cfg.boost_rounds <= 1024
+                       and slot_image_bytes(spec.n_dates, cfg.boost_rounds, F, fast) <= _SLOT_IMAGE_LIMIT)
+    if device_loop:
+        if torch is None:
+            raise RuntimeError("device_loop=True needs a CUDA device")
+        return _build_device_loop(params, spec, cfg, seed, sampler, mode, shard, torch, stream, mp, F, call_like)
     for m in range(spec.n_dates - 1, 0, -1):
         later = rule.pack()
         bridge = bridge_scalars(params, spec, m)

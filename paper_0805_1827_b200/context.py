@@ -54,7 +54,7 @@ def default_device() -> int:
 class Context:
     """One brm_ctx: market + rule image on one device in one precision mode."""
 
-    def __init__(self, mp, rp, device: int | None = None, mode=None):
+    def __init__(self, mp, rp, device: int | None = None, mode=None, capacity: int | None = None):
         self.device = default_device() if device is None else int(device)
         self.mode = resolve_mode(mode)
         self.d = int(mp.d)
@@ -80,10 +80,28 @@ class Context:
                         arr(rp.cmc_starts, np.int32), arr(rp.cmc_counts, np.int32), arr(feat, np.int32),
                         arr(rp.cmc_thr), arr(rp.cmc_pol), arr(rp.cmc_alpha), arr(rp.cmc_intercept))
         handle = C.c_void_p()
-        N.check(N.lib.brm_ctx_create(C.byref(md), C.byref(rd), self.device, self.mode, C.byref(handle)))
+        if capacity is not None:
+            # slotted CMC image, every date empty; dates are filled on the device
+            N.check(N.lib.brm_ctx_create_cmc(C.byref(md), self.call_like, int(capacity), self.device, self.mode,
+                                             C.byref(handle)))
+        else:
+            N.check(N.lib.brm_ctx_create(C.byref(md), C.byref(rd), self.device, self.mode, C.byref(handle)))
         self.handle = handle
         self._finalizer = weakref.finalize(self, N.lib.brm_ctx_destroy, handle)
         self._normals = None
+
+    @classmethod
+    def cmc_slots(cls, mp, call_like: bool, capacity: int, device: int | None = None, mode=None) -> "Context":
+        """Device-resident CMC rule image (brm_ctx_create_cmc): room for
+        ``capacity`` stumps per date, filled by :meth:`set_ensemble`."""
+        from .packs import RulePack
+        return cls(mp, RulePack.european(call_like), device, mode, capacity=capacity)
+
+    def set_ensemble(self, m: int, feat, thr, pol, alpha, count, intercept) -> None:
+        """Write date m's ensemble (device tensors sized [capacity], count and
+        intercept as 1-element tensors) into the image, on the context's stream."""
+        N.check(N.lib.brm_ctx_set_ensemble(self.handle, int(m), N.ptr(feat), N.ptr(thr), N.ptr(pol), N.ptr(alpha),
+                                           N.ptr(count), N.ptr(intercept)))
 
     def close(self) -> None:
         self._finalizer()

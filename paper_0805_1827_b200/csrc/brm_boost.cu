@@ -174,7 +174,8 @@ struct BoostParams {
   int *out_feat;
   double *out_thr, *out_pol, *out_alpha, *out_err;
   int *out_count;
-  int n_pos;
+  double *out_intercept;
+  const int *n_pos;        // positives in the training set (device)
   int raw;  // 1: one fit_stump search with the given weights, no boosting rules
   long long *timing;  // optional per-phase clock64 totals of CTA 0 (diagnostics)
 };
@@ -294,6 +295,23 @@ __device__ __forceinline__ void gather_tile(const double *__restrict__ w, const 
   }
 }
 
+// One class (boosting.py:185-187): a zero-round ensemble carrying the class
+// sign; decided on the device so a fit needs no host round trip.
+__device__ __forceinline__ bool one_class_exit(int raw, int n, int n_pos, int *out_count, double *out_intercept) {
+  if (raw || (n_pos != 0 && n_pos != n)) return false;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *out_count = 0;
+    *out_intercept = n_pos == n ? 1.0 : -1.0;
+  }
+  return true;
+}
+
+// No stump beat random guessing: the majority sign (boosting.py:202-205).
+__device__ __forceinline__ void write_result(int count, int n, int n_pos, int *out_count, double *out_intercept) {
+  *out_count = count;
+  *out_intercept = count > 0 ? 0.0 : (2 * n_pos >= n ? 1.0 : -1.0);
+}
+
 struct Cand {
   double err;
   int key;  // 2*i + (minus polarity)
@@ -356,6 +374,8 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
 
   const int n = P.n, F = P.F;
   const int f = blockIdx.x;
+  const int n_pos_all = *P.n_pos;
+  if (one_class_exit(P.raw, n, n_pos_all, P.out_count, P.out_intercept)) return;
   // reweighting slices are whole pairwise leaves, so each CTA also publishes
   // the leaf sums of the new weights and sum(w) needs only the tree combine
   const int L = P.n_leaves;
@@ -399,7 +419,7 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
       const int *nid = P.neg_idx + (size_t)f * n;
       double *pc = P.pcum + (size_t)f * n;
       double *nc = P.ncum + (size_t)f * n;
-      const int n_pos = P.n_pos, n_neg = n - P.n_pos;
+      const int n_pos = n_pos_all, n_neg = n - n_pos_all;
       double pacc = 0.0, nacc = 0.0;  // np.cumsum(where(y>0, w, 0)): zeros never change a partial sum
       // tiles: all threads gather, the two highest warps run the two sequential
       // chains (the issue arbiter favours high warp ids), all threads write back
@@ -580,7 +600,7 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
     grid.sync();
     if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[6] += now - t_mark; t_mark = now; }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *P.out_count = count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) write_result(count, n, n_pos_all, P.out_count, P.out_intercept);
 }
 
 // Per feature: ids of positives / negatives in sorted order and the running
@@ -636,6 +656,8 @@ struct FastBoostParams {
   int *out_feat;
   double *out_thr, *out_pol, *out_alpha, *out_err;
   int *out_count;
+  double *out_intercept;
+  const int *n_pos;  // positives in the training set (device)
 };
 
 // Fixed-order CTA sum (thread-strided runs, shuffle tree, warps in order).
@@ -668,6 +690,8 @@ __global__ void __launch_bounds__(kBoostThreads) boost_fast_kernel(FastBoostPara
   const int n = P.n, F = P.F, f = blockIdx.x;
   const int slice = (n + gridDim.x - 1) / gridDim.x;
   const int w_lo = blockIdx.x * slice, w_hi = min(w_lo + slice, n);
+  const int n_pos_all = *P.n_pos;
+  if (one_class_exit(P.raw, n, n_pos_all, P.out_count, P.out_intercept)) return;
   int count = 0;
   for (int round = 0; round < P.rounds; ++round) {
     const double ssum = cta_sum_fixed(P.w, n, s_red);
@@ -804,7 +828,7 @@ __global__ void __launch_bounds__(kBoostThreads) boost_fast_kernel(FastBoostPara
     }
     grid.sync();
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *P.out_count = count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) write_result(count, n, n_pos_all, P.out_count, P.out_intercept);
 }
 
 __global__ void transpose_cols(const double *xs, int n, int F, double *xt, int *iota) {
@@ -978,7 +1002,11 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
                                 int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha,
                                 double *out_err, int32_t *out_count, double *out_intercept) {
   const bool raw = flags & BRM_FIT_SINGLE_STUMP;
+  const bool dev_out = flags & BRM_FIT_DEVICE_RESULT;
   if (!xs || !betas || !out_count || !out_intercept) return bfail(BRM_EINVAL, "NULL argument");
+  if (dev_out && !(is_dev(out_feat) && is_dev(out_thr) && is_dev(out_pol) && is_dev(out_alpha) && is_dev(out_err) &&
+                   is_dev(out_count) && is_dev(out_intercept)))
+    return bfail(BRM_EINVAL, "BRM_FIT_DEVICE_RESULT needs device output pointers");
   if (rounds < 1) return bfail(BRM_EINVAL, "need at least one round, got " + std::to_string(rounds));
   if (n64 < 1 || n64 > (1 << 26)) return bfail(BRM_EINVAL, "training set size out of range");
   if (F < 1 || F > 148) return bfail(BRM_EINVAL, "feature count out of range");
@@ -1016,9 +1044,11 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       labels_from_betas<<<(n + 255) / 256, 256, 0, s>>>(d_b, n, d_y, d_npos);
       prof_end(tok, s);
     }
-    BCU(cudaMemcpyAsync(&npos, d_npos, sizeof(int), cudaMemcpyDeviceToHost, s));
-    BCU(cudaStreamSynchronize(s));
-    if (!raw && (npos == 0 || npos == n)) {
+    if (!dev_out) {  // (device results: the kernel itself handles one class)
+      BCU(cudaMemcpyAsync(&npos, d_npos, sizeof(int), cudaMemcpyDeviceToHost, s));
+      BCU(cudaStreamSynchronize(s));
+    }
+    if (!dev_out && !raw && (npos == 0 || npos == n)) {
       // one class: zero-round ensemble carrying the class sign (boosting.py:185-187)
       *out_count = 0;
       *out_intercept = npos == n ? 1.0 : -1.0;
@@ -1075,6 +1105,17 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
     BCU(S.get(&d_alpha, rounds));
     BCU(S.get(&d_rerr, rounds));
     BCU(S.get(&d_count, 1));
+    double *d_icept;
+    BCU(S.get(&d_icept, 1));
+    if (dev_out) {  // the kernel writes the caller's arrays
+      d_feat = out_feat;
+      d_thr = out_thr;
+      d_pol = out_pol;
+      d_alpha = out_alpha;
+      d_rerr = out_err;
+      d_count = out_count;
+      d_icept = out_intercept;
+    }
     root = pw_tree(n, tree);
     double *d_leafsum;
     BCU(S.get(&d_leafsum, tree.leaves.size()));
@@ -1094,7 +1135,6 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       P.F = F;
       P.rounds = rounds;
       P.raw = raw ? 1 : 0;
-      P.n_pos = npos;
       P.xs = d_xs;
       P.xsorted = d_xsorted;
       P.xt = d_xt;
@@ -1123,6 +1163,8 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       P.out_alpha = d_alpha;
       P.out_err = d_rerr;
       P.out_count = d_count;
+      P.out_intercept = d_icept;
+      P.n_pos = d_npos;
       long long *d_timing = nullptr;
       const bool timing = getenv("BRM_BOOST_TIMING") != nullptr;
       if (timing) {
@@ -1163,6 +1205,8 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
         Q.out_alpha = d_alpha;
         Q.out_err = d_rerr;
         Q.out_count = d_count;
+        Q.out_intercept = d_icept;
+        Q.n_pos = d_npos;
         void *qargs[] = {&Q};
         BCU(cudaLaunchCooperativeKernel((void *)boost_fast_kernel, dim3(F), dim3(kBoostThreads), qargs, 0, s));
       } else {
@@ -1179,27 +1223,26 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       }
     }
     BCU(cudaGetLastError());
-    {
+    if (!dev_out) {
       int count = 0;
+      double icept = 0.0;
       BCU(cudaMemcpyAsync(&count, d_count, sizeof(int), cudaMemcpyDeviceToHost, s));
+      BCU(cudaMemcpyAsync(&icept, d_icept, sizeof(double), cudaMemcpyDeviceToHost, s));
       BCU(cudaStreamSynchronize(s));
       *out_count = count;
+      *out_intercept = icept;
       if (count > 0) {
         BCU(cudaMemcpyAsync(out_feat, d_feat, sizeof(int) * count, cudaMemcpyDefault, s));
         BCU(cudaMemcpyAsync(out_thr, d_thr, sizeof(double) * count, cudaMemcpyDefault, s));
         BCU(cudaMemcpyAsync(out_pol, d_pol, sizeof(double) * count, cudaMemcpyDefault, s));
         BCU(cudaMemcpyAsync(out_alpha, d_alpha, sizeof(double) * count, cudaMemcpyDefault, s));
         BCU(cudaMemcpyAsync(out_err, d_rerr, sizeof(double) * count, cudaMemcpyDefault, s));
-        *out_intercept = 0.0;
         count_transfer(0, (sizeof(int) + 4 * sizeof(double)) * count);
-      } else {
-        // no stump beat random guessing: majority sign (boosting.py:202-205)
-        *out_intercept = 2 * npos >= n ? 1.0 : -1.0;
       }
     }
   }
 done:
-  cudaStreamSynchronize(s);
+  if (!dev_out) cudaStreamSynchronize(s);
   if (prev >= 0) cudaSetDevice(prev);
   return rc;
 }

@@ -224,6 +224,8 @@ struct brm_ctx {
   double *normals = nullptr;  // supplied-normals copy (device)
   cudaEvent_t ready = nullptr;  // image upload complete (waited on by every launch stream)
   uint64_t nrm_base = 0, nrm_count = 0;
+  int capacity = 0;  // > 0: slotted CMC image (brm_ctx_create_cmc)
+  SlotDims slot{};
   cudaStream_t stream() const { return has_user_stream ? user_stream : own_stream; }
   bool fast() const { return mode == BRM_MODE_FAST; }
   const double *blob_dbl(int off) const { return reinterpret_cast<const double *>(blob) + off; }
@@ -352,8 +354,15 @@ int brm_device_count(int32_t *count) {
   return BRM_OK;
 }
 
-int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t device, int32_t mode,
-                   brm_ctx **out) {
+}  // extern "C"
+
+namespace {
+
+// capacity > 0: a CMC image with a fixed slot of `capacity` stumps (and the
+// matching step-table space) per date, every date empty; brm_ctx_set_ensemble
+// then fills dates on the device.  capacity == 0: the image of `rl`.
+int ctx_create_impl(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t device, int32_t mode,
+                    int32_t capacity, brm_ctx **out) {
   if (!mk || !rl || !out) return fail(BRM_EINVAL, "NULL argument");
   *out = nullptr;
   int ndev = 0;
@@ -453,17 +462,41 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
   h.o_izhi = put(izhi, std::max(k, 1));
   if (icept.empty()) icept.assign(nd + 1, -1.0);
   h.o_icept = put(icept, nd + 1);
-  h.o_thr = put(thr, 1);
   std::vector<double> ap(ns);
   for (int t = 0; t < ns; ++t) ap[t] = alpha[t] * pol[t];  // the product the reference forms per vote
-  h.o_ap = put(ap, 1);
   // per (date, feature) step tables of the stump score (see cmc_stop in brm_model.cuh)
   const int nfeat = d > 1 ? d + 1 : 1;
   h.nfeat = nfeat;
   std::vector<double> tt, tv, bound(nd + 1, 0.0);
   std::vector<int32_t> toff((size_t)(nd + 1) * nfeat, 0), tcnt((size_t)(nd + 1) * nfeat, 0),
       voff((size_t)(nd + 1) * nfeat, 0);
-  for (int m = 0; m <= nd; ++m) {
+  const SlotDims slot = slot_dims(capacity, nfeat);
+  if (capacity > 0) {
+    // slotted image: date m owns stumps [m R, m R + R), thresholds
+    // [m TS, m TS + TS) and table values [m VS, m VS + VS); empty dates have
+    // one zero-valued table entry per feature and the intercept -1
+    const size_t R = (size_t)capacity;
+    thr.assign((nd + 1) * R, 0.0);
+    ap.assign((nd + 1) * R, 0.0);
+    feat.assign((nd + 1) * R, 0);
+    starts.assign(nd + 1, 0);
+    counts.assign(nd + 1, 0);
+    icept.assign(nd + 1, -1.0);
+    for (int m = 0; m <= nd; ++m) starts[m] = (int32_t)(m * R);
+    tt.assign((size_t)(nd + 1) * slot.ts, std::numeric_limits<double>::infinity());
+    tv.assign((size_t)(nd + 1) * slot.vs, 0.0);
+    for (int m = 0; m <= nd; ++m) {
+      for (int f = 0; f < nfeat; ++f) {
+        toff[(size_t)m * nfeat + f] = m * slot.ts;
+        tcnt[(size_t)m * nfeat + f] = 1;
+        voff[(size_t)m * nfeat + f] = m * slot.vs + f;
+      }
+      bound[m] = 4.0 * (double)(nfeat + 4) * std::ldexp(1.0, -53) + 1e-300;
+    }
+  }
+  h.o_thr = put(thr, 1);
+  h.o_ap = put(ap, 1);
+  for (int m = 0; m <= nd && capacity == 0; ++m) {
     const int t0 = rl->kind == BRM_RULE_CMC ? starts[m] : 0, cnt = rl->kind == BRM_RULE_CMC ? counts[m] : 0;
     double absum = rl->kind == BRM_RULE_CMC ? std::fabs(icept[m]) : 0.0;
     for (int f = 0; f < nfeat; ++f) {
@@ -547,8 +580,71 @@ int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t d
     brm_ctx_destroy(c);
     return fail(BRM_EINVAL, "model image (%d B) exceeds shared memory", smem_model(c));
   }
+  c->capacity = capacity;
+  c->slot = slot;
   *out = c;
   return BRM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int brm_ctx_create(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t device, int32_t mode,
+                   brm_ctx **out) {
+  return ctx_create_impl(mk, rl, device, mode, 0, out);
+}
+
+int brm_ctx_create_cmc(const brm_market_desc *mk, int32_t call_like, int32_t capacity, int32_t device, int32_t mode,
+                       brm_ctx **out) {
+  if (capacity < 1 || capacity > kMaxSlotStumps)
+    return fail(BRM_EINVAL, "stump capacity %d outside 1..%d", capacity, kMaxSlotStumps);
+  brm_rule_desc rl{};
+  rl.kind = BRM_RULE_CMC;
+  rl.call_like = call_like ? 1 : 0;
+  rl.imm_date = -1;
+  rl.nbasis = 1;
+  rl.n_stumps = 0;
+  // an empty rule: every date without an ensemble (starts / counts / intercepts
+  // are rebuilt in slotted form, so these only have to pass validation)
+  const int nd = mk ? mk->n_dates : 0;
+  std::vector<int32_t> zeros(std::max(nd + 1, 1), 0);
+  std::vector<double> icept(std::max(nd + 1, 1), -1.0);
+  rl.cmc_starts = zeros.data();
+  rl.cmc_counts = zeros.data();
+  rl.cmc_intercept = icept.data();
+  return ctx_create_impl(mk, &rl, device, mode, capacity, out);
+}
+
+int brm_ctx_set_ensemble(brm_ctx *c, int32_t date, const int32_t *feat, const double *thr, const double *pol,
+                         const double *alpha, const int32_t *count, const double *intercept) {
+  if (!c) return fail(BRM_EINVAL, "NULL context");
+  if (c->capacity <= 0) return fail(BRM_EINVAL, "context was not created by brm_ctx_create_cmc");
+  if (date < 1 || date >= c->hdr.n_dates)
+    return fail(BRM_EINVAL, "ensemble date %d outside 1..%d", date, c->hdr.n_dates - 1);
+  if (!feat || !thr || !pol || !alpha || !count || !intercept) return fail(BRM_EINVAL, "NULL argument");
+  DeviceScope scope(c->device);
+  const cudaStream_t s = c->stream();
+  BRM_CUDA(cudaStreamWaitEvent(s, c->ready, 0));
+  const int R = c->capacity;
+  Call call(s);
+  const int32_t *d_feat, *d_count;
+  const double *d_thr, *d_pol, *d_alpha, *d_icept;
+  BRM_TRY(call.in(feat, R, &d_feat));
+  BRM_TRY(call.in(thr, R, &d_thr));
+  BRM_TRY(call.in(pol, R, &d_pol));
+  BRM_TRY(call.in(alpha, R, &d_alpha));
+  BRM_TRY(call.in(count, 1, &d_count));
+  BRM_TRY(call.in(intercept, 1, &d_icept));
+  const int tok = prof_begin(PK_AUX, s);
+  void *args[] = {(void *)&c->blob, (void *)&c->hdr, (void *)&date, (void *)&R, (void *)&c->slot,
+                  (void *)&d_feat, (void *)&d_thr, (void *)&d_pol, (void *)&d_alpha, (void *)&d_count,
+                  (void *)&d_icept};
+  BRM_TRY(allow_smem(set_ensemble_kernel(), (int)set_ensemble_smem(R)));
+  BRM_CUDA(cudaLaunchKernel(set_ensemble_kernel(), dim3(1), dim3(256), args, set_ensemble_smem(R), s));
+  prof_end(tok, s);
+  BRM_CUDA(cudaEventRecord(c->ready, s));  // later launches on any stream see the new date
+  return call.finish();
 }
 
 int brm_ctx_destroy(brm_ctx *c) {

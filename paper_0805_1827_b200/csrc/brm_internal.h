@@ -5,6 +5,8 @@
 
 #include "brm_model.cuh"
 
+#include <algorithm>
+
 namespace brm {
 
 constexpr int kWalkThreads = 256;   // threads per walker CTA
@@ -104,6 +106,19 @@ void *sample_kernel();
 void *fill_raw_kernel();
 void *fill_normals_kernel();
 void *math_selftest_kernel();
+// Slotted CMC images (brm_ctx_create_cmc): per date, `ts` threshold entries
+// and `vs` table values.  Each feature's padded threshold list has at most
+// 2 u_f entries (u_f distinct thresholds, padded to a power of two minus one)
+// and u_f + 1 values, so ts = 2 R and vs = R + F bound any ensemble of at most
+// R stumps on F features.
+struct SlotDims {
+  int ts, vs;
+};
+inline SlotDims slot_dims(int capacity, int nfeat) { return SlotDims{std::max(2 * capacity, 1), capacity + nfeat}; }
+constexpr int kMaxSlotStumps = 1024;
+void *set_ensemble_kernel();
+size_t set_ensemble_smem(int capacity);
+
 // Keep freed stream-ordered allocations in the device's default pool across
 // synchronisations (the pool's default release threshold of 0 hands them back
 // to the driver at every sync, and the next call re-maps them).

@@ -143,6 +143,137 @@ KernelTriple kernels_for(int d, bool fast) {
   }
 }
 
+// ---- device-side ensemble upload (slotted CMC images) --------------------
+// Double-double accumulation for the step-table values: the host build sums
+// in long double; either is far inside the rounding bound that guards the
+// table decision (cmc_stop), so decisions stay exact.
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  const double s = __dadd_rn(a.hi, b.hi), bb = __dsub_rn(s, a.hi);
+  double e = __dadd_rn(__dsub_rn(a.hi, __dsub_rn(s, bb)), __dsub_rn(b.hi, bb));
+  const double t = __dadd_rn(a.lo, b.lo), bt = __dsub_rn(t, a.lo);
+  const double f = __dadd_rn(__dsub_rn(a.lo, __dsub_rn(t, bt)), __dsub_rn(b.lo, bt));
+  e = __dadd_rn(e, t);
+  double hi = __dadd_rn(s, e);
+  e = __dsub_rn(e, __dsub_rn(hi, s));
+  e = __dadd_rn(e, f);
+  const double h2 = __dadd_rn(hi, e);
+  return DD{h2, __dsub_rn(e, __dsub_rn(h2, hi))};
+}
+
+// Writes date m's ensemble (count and intercept read on the device) into its
+// slot: stumps, the per-feature sorted thresholds padded with +inf to a power
+// of two minus one, the step-table values and the rounding bound -- the same
+// image brm_ctx_create builds on the host (brm_capi.cu).
+__global__ void __launch_bounds__(256) set_ensemble(unsigned char *blob, ModelHdr h, int m, int R, SlotDims slot,
+                                                    const int32_t *feat, const double *thr, const double *pol,
+                                                    const double *alpha, const int32_t *count,
+                                                    const double *intercept) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *s_thr = reinterpret_cast<double *>(smem_raw);
+  double *s_ap = s_thr + R;
+  double *s_hi = s_ap + R;               // [8][R] per-warp rank sums (double-double)
+  double *s_lo = s_hi + 8 * R;
+  int *s_feat = reinterpret_cast<int *>(s_lo + 8 * R);
+  int *s_rank = s_feat + R;              // rank r among the feature's distinct thresholds (-1-r: repeat)
+  int *s_first = s_rank + R;
+  __shared__ int s_u[kMaxD + 1], s_toff[kMaxD + 1], s_voff[kMaxD + 1], s_p[kMaxD + 1];
+  double *gd = reinterpret_cast<double *>(blob);
+  int32_t *gi = reinterpret_cast<int32_t *>(blob + 8 * (size_t)h.n_dbl);
+  const int F = h.nfeat;
+  const int c = max(0, min(*count, R));
+  const double ic = *intercept;
+  for (int t = threadIdx.x; t < c; t += blockDim.x) {
+    s_thr[t] = thr[t];
+    s_ap[t] = __dmul_rn(alpha[t], pol[t]);  // the product the reference forms per vote
+    s_feat[t] = feat[t];
+  }
+  for (int f = threadIdx.x; f < F; f += blockDim.x) s_u[f] = 0;
+  __syncthreads();
+  // distinct thresholds per feature (first occurrence in stump order) and
+  // their ranks (c <= R stumps: O(c^2) compares)
+  for (int t = threadIdx.x; t < c; t += blockDim.x) {
+    const int f = s_feat[t];
+    const double x = s_thr[t];
+    bool first = true;
+    for (int q = 0; q < t && first; ++q) first = !(s_feat[q] == f && s_thr[q] == x);
+    s_first[t] = first;
+    if (first) atomicAdd(&s_u[f], 1);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < c; t += blockDim.x) {
+    const int f = s_feat[t];
+    const double x = s_thr[t];
+    int r = 0;
+    for (int q = 0; q < c; ++q) r += s_first[q] && s_feat[q] == f && s_thr[q] < x;
+    s_rank[t] = s_first[t] ? r : -1 - r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int to = m * slot.ts, vo = m * slot.vs;
+    for (int f = 0; f < F; ++f) {
+      int P = 1;
+      while (P < s_u[f] + 1) P <<= 1;
+      s_p[f] = P;
+      s_toff[f] = to;
+      s_voff[f] = vo;
+      gi[h.o_toff + m * F + f] = to;
+      gi[h.o_tcnt + m * F + f] = P;
+      gi[h.o_voff + m * F + f] = vo;
+      to += P - 1;
+      vo += s_u[f] + 1;
+    }
+    gi[h.o_counts + m] = c;
+    gd[h.o_icept + m] = ic;
+    double absum = fabs(ic);
+    for (int t = 0; t < c; ++t) absum = __dadd_rn(absum, fabs(s_ap[t]));
+    gd[h.o_bound + m] = __dadd_rn(__dmul_rn(4.0 * (double)(c + F + 4), ldexp(absum, -53)), 1e-300);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < c; t += blockDim.x) {
+    gd[h.o_thr + m * R + t] = s_thr[t];
+    gd[h.o_ap + m * R + t] = s_ap[t];
+    gi[h.o_feat + m * R + t] = s_feat[t];
+    if (s_rank[t] >= 0) gd[h.o_tt + s_toff[s_feat[t]] + s_rank[t]] = s_thr[t];
+  }
+  for (int f = 0; f < F; ++f)
+    for (int k = s_u[f] + threadIdx.x; k < s_p[f] - 1; k += blockDim.x)
+      gd[h.o_tt + s_toff[f] + k] = __longlong_as_double(0x7ff0000000000000LL);
+  // table values: T[0] = -sum(ap), T[k+1] = T[k] + 2 * (votes of rank k), one warp per feature
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *whi = s_hi + warp * R, *wlo = s_lo + warp * R;
+  for (int f = warp; f < F; f += blockDim.x >> 5) {
+    const int u = s_u[f];
+    for (int k = lane; k < u; k += 32) {
+      DD acc{0.0, 0.0};
+      for (int t = 0; t < c; ++t) {
+        const int rk = s_rank[t] >= 0 ? s_rank[t] : -1 - s_rank[t];
+        if (s_feat[t] == f && rk == k) acc = dd_add(acc, DD{s_ap[t], 0.0});
+      }
+      whi[k] = acc.hi;
+      wlo[k] = acc.lo;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      DD acc{0.0, 0.0};
+      for (int t = 0; t < c; ++t)
+        if (s_feat[t] == f) acc = dd_add(acc, DD{-s_ap[t], 0.0});
+      double *tv = gd + h.o_tv + s_voff[f];
+      tv[0] = __dadd_rn(acc.hi, acc.lo);
+      for (int k = 0; k < u; ++k) {
+        acc = dd_add(acc, DD{2.0 * whi[k], 2.0 * wlo[k]});
+        tv[k + 1] = __dadd_rn(acc.hi, acc.lo);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+size_t set_ensemble_smem(int capacity) { return (size_t)capacity * (2 * 8 + 16 * 8 + 3 * 4); }
+void *set_ensemble_kernel() { return (void *)&set_ensemble; }
+
 void *finish_kernel() { return (void *)&finish_units; }
 void *sample_kernel() { return (void *)&sample_points; }
 void *fill_raw_kernel() { return (void *)&fill_raw; }
