@@ -218,10 +218,11 @@ __device__ __forceinline__ void pw_leaf_sums(const PwView &T, const double *a, i
     double tv = j < tail ? a[off + main + j] : 0.0;
     // the 16 mapped values are independent: form them all before the
     // dependent adds so their loads / divisions overlap
+    // op runs on every slot (masked slots read element `off` and map a zero):
+    // branch-free, so the loads and dependency chains of all slots overlap
 #pragma unroll
-    for (int q = 0; q < kPwBlock / 8; ++q)
-      if (8 * q < main) col[q] = op(off + 8 * q + j, col[q]);
-    if (j < tail) tv = op(off + main + j, tv);
+    for (int q = 0; q < kPwBlock / 8; ++q) col[q] = op(8 * q < main ? off + 8 * q + j : off, col[q]);
+    tv = op(j < tail ? off + main + j : off, tv);
 #pragma unroll
     for (int q = 0; q < kPwBlock / 8; ++q)
       if (8 * q < main) sink(off + 8 * q + j, col[q]);
@@ -395,10 +396,19 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
   const int l_lo = (int)((long long)blockIdx.x * L / gridDim.x), l_hi = (int)((long long)(blockIdx.x + 1) * L / gridDim.x);
   double *wn = P.wn + (size_t)f * n;
   int count = 0;
-  long long t_mark = 0;
+  // per-phase clock totals (diagnostics, BRM_BOOST_TIMING): thread 0 of CTA 0,
+  // slot 7 the positive-chain thread; kept in registers, stored at the end
+  const bool timed = P.timing && blockIdx.x == 0;
+  long long t_mark = 0, tacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#define BRM_TSLOT(k)                       \
+  if (timed && threadIdx.x == 0) {         \
+    const long long now_ = clock64();      \
+    tacc[k] += now_ - t_mark;              \
+    t_mark = now_;                         \
+  }
 
   for (int round = 0; round < P.rounds; ++round) {
-    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) t_mark = clock64();
+    if (timed && threadIdx.x == 0) t_mark = clock64();
     // ---- wn = w / w.sum() (numpy pairwise order), CTA-private copy, and
     // total = wn.sum() in the same pass ----------------------------------
     double total;
@@ -408,11 +418,13 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
     } else {
       for (int l = threadIdx.x; l < L; l += blockDim.x) s_node[l] = __ldcg(P.leafsum + l);
       const double s = pw_tree_sum(T, s_node);
+      if (timed && threadIdx.x == 0) tacc[9] += clock64() - t_mark;
       pw_leaf_sums(
           T, P.w, 0, L, s_node, [&](int, double x) { return div_nb(x, s); }, [&](int i, double v) { wn[i] = v; });
+      if (timed && threadIdx.x == 0) tacc[10] += clock64() - t_mark;
       total = pw_tree_sum(T, s_node);
     }
-    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[1] += now - t_mark; t_mark = now; }
+    BRM_TSLOT(1);
     // ---- split search on feature f -------------------------------------
     if (f < F) {
       const int *pid = P.pos_idx + (size_t)f * n;
@@ -430,9 +442,9 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
         gather_tile(wn, nid + t0, tn, s_in_n);
         __syncthreads();
         if (threadIdx.x == chain_p) {
-          const long long c0 = P.timing ? clock64() : 0;
+          const long long c0 = timed ? clock64() : 0;
           serial_chain(s_in_p, s_out_p, tp, pacc);
-          if (P.timing && blockIdx.x == 0) P.timing[7] += clock64() - c0;
+          if (timed) tacc[7] += clock64() - c0;
         }
         else if (threadIdx.x == chain_n) serial_chain(s_in_n, s_out_n, tn, nacc);
         __syncthreads();
@@ -440,7 +452,7 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
         for (int j = threadIdx.x; j < tn; j += blockDim.x) nc[t0 + j] = s_out_n[j];
       }
       __syncthreads();
-    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[2] += now - t_mark; t_mark = now; }
+    BRM_TSLOT(2);
       // split points: brk[i] = (positives up to i) - 1, (negatives up to i) - 1,
       // precomputed once per fit; x == INT_MIN marks "no distinct-value break"
       const int2 *brk = P.brk + (size_t)f * n;
@@ -487,9 +499,9 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
         P.feat_pos[f] = best.key;
       }
     }
-    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[3] += now - t_mark; t_mark = now; }
+    BRM_TSLOT(3);
     grid.sync();
-    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[4] += now - t_mark; t_mark = now; }
+    BRM_TSLOT(4);
     // ---- pick the winner (every CTA, same answer) ------------------------
     // first minimum over features in order: (err, feature) lexicographic
     double be = __longlong_as_double(0x7ff0000000000000LL);
@@ -582,12 +594,13 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
     if (s_stop == 1) break;
     ++count;
     if (s_stop == 3 || round + 1 == P.rounds) break;
-    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[5] += now - t_mark; t_mark = now; }
+    BRM_TSLOT(5);
     // ---- reweight own slice: w = (w / sum) * exp(-alpha * y * pred) ------
     {
       const double a = s_alpha, thr = s_thr, pol = s_pol;
       const int feat = s_feat;
       const double e_agree = exp(-a), e_miss = exp(a);
+      if (timed && threadIdx.x == 0) tacc[8] += clock64() - t_mark;
       pw_leaf_sums(
           T, wn, l_lo, l_hi, P.leafsum,
           [&](int i, double x) {
@@ -596,11 +609,16 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
           },
           [&](int i, double v) { P.w[i] = v; });
     }
-    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) P.timing[0] += clock64() - t_mark;
+    if (timed && threadIdx.x == 0) tacc[0] += clock64() - t_mark;
     grid.sync();
-    if (P.timing && blockIdx.x == 0 && threadIdx.x == 0) { const long long now = clock64(); P.timing[6] += now - t_mark; t_mark = now; }
+    BRM_TSLOT(6);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) write_result(count, n, n_pos_all, P.out_count, P.out_intercept);
+  if (timed && threadIdx.x == 0)
+    for (int k = 0; k < 12; ++k)
+      if (k != 7) P.timing[k] = tacc[k];
+  if (timed && threadIdx.x == blockDim.x - 64) P.timing[7] = tacc[7];
+#undef BRM_TSLOT
 }
 
 // Per feature: ids of positives / negatives in sorted order and the running
@@ -1168,8 +1186,8 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       long long *d_timing = nullptr;
       const bool timing = getenv("BRM_BOOST_TIMING") != nullptr;
       if (timing) {
-        BCU(S.get(&d_timing, 8));
-        BCU(cudaMemsetAsync(d_timing, 0, 8 * sizeof(long long), s));
+        BCU(S.get(&d_timing, 12));
+        BCU(cudaMemsetAsync(d_timing, 0, 12 * sizeof(long long), s));
       }
       P.timing = d_timing;
       int smem_max = 0;
@@ -1214,12 +1232,14 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       }
       prof_end(tok, s);
       if (timing) {
-        long long h[8];
+        long long h[12];
         BCU(cudaMemcpyAsync(h, d_timing, sizeof h, cudaMemcpyDeviceToHost, s));
         BCU(cudaStreamSynchronize(s));
         fprintf(stderr, "boost phases (kcycles, CTA 0): norm+total %.0f chains %.0f (positive chain alone %.0f) scan %.0f "
                 "sync1 %.0f pick %.0f reweight+sync2 %.0f (reweight alone %.0f)\n",
                 h[1] / 1e3, h[2] / 1e3, h[7] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, h[6] / 1e3, h[0] / 1e3);
+        fprintf(stderr, "  sub-phases (kcycles): [8] %.0f [9] %.0f [10] %.0f [11] %.0f\n", h[8] / 1e3, h[9] / 1e3,
+                h[10] / 1e3, h[11] / 1e3);
       }
     }
     BCU(cudaGetLastError());
