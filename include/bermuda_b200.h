@@ -132,8 +132,9 @@ int brm_raw_uint64(int32_t device, uint64_t key64, uint64_t stream64, uint64_t s
 int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t start, int64_t count,
                 double *out);
 
-/* Self-test of the walker's branch-free fp64 exp / divide against CUDA's
- * exp / __ddiv_rn (kind 0 exp_nb(a), 1 exp(a), 2 div_nb(a, b), 3 a / b). */
+/* Self-test of the walker's branch-free fp64 exp / divide / log / sqrt against
+ * CUDA's exp / __ddiv_rn / log / __dsqrt_rn (kind 0 exp_nb(a), 1 exp(a),
+ * 2 div_nb(a, b), 3 a / b, 4 log_nb(a), 5 log(a), 6 sqrt_nb(a), 7 sqrt(a)). */
 int brm_selftest_math(int32_t device, int32_t kind, const double *a, const double *b, int64_t n, double *out);
 
 /* ---- Path walker ------------------------------------------------------- */

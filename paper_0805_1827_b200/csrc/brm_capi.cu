@@ -441,6 +441,9 @@ int ctx_create_impl(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t 
     for (int a = 0; a < d; ++a)
       if (a != i && chol[i * d + a] != 0.0) diag = 0;
   h.chol_lower = diag ? 2 : lower;
+  h.unit_diag = diag;
+  for (int i = 0; i < d; ++i)
+    if (chol[i * d + i] != 1.0) h.unit_diag = 0;
   std::vector<double> dbl;
   auto put = [&](const std::vector<double> &v, size_t min_len) {
     int off = (int)dbl.size();
@@ -729,13 +732,13 @@ int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t star
 
 int brm_selftest_math(int32_t device, int32_t kind, const double *a, const double *b, int64_t n, double *out) {
   if (n <= 0) return BRM_OK;
-  if (kind < 0 || kind > 3) return fail(BRM_EINVAL, "unknown self-test %d", kind);
+  if (kind < 0 || kind > 7) return fail(BRM_EINVAL, "unknown self-test %d", kind);
   DeviceScope scope(device);
   Call call(nullptr);
   const double *da, *db = nullptr;
   double *o;
   BRM_TRY(call.in(a, n, &da));
-  if (kind >= 2) BRM_TRY(call.in(b, n, &db));
+  if (kind == 2 || kind == 3) BRM_TRY(call.in(b, n, &db));
   BRM_TRY(call.out(out, n, &o));
   void *args[] = {&kind, &da, &db, &n, &o};
   BRM_CUDA(cudaLaunchKernel(math_selftest_kernel(), dim3((unsigned)((n + 255) / 256)), dim3(256), args, 0, call.stream));

@@ -110,7 +110,7 @@ __global__ void fill_normals(uint64_t key, uint64_t stream, uint64_t start, int6
     out[i] = normal_at(key, stream, start + (uint64_t)i);
 }
 
-// Math self-test: the branch-free exp / divide against the library functions.
+// Math self-test: the branch-free exp / divide / log / sqrt against the library functions.
 __global__ void math_selftest(int kind, const double *a, const double *b, int64_t n, double *out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -118,7 +118,11 @@ __global__ void math_selftest(int kind, const double *a, const double *b, int64_
     case 0: out[i] = exp_nb(a[i]); break;
     case 1: out[i] = exp(a[i]); break;
     case 2: out[i] = div_nb(a[i], b[i]); break;
-    default: out[i] = __ddiv_rn(a[i], b[i]); break;
+    case 3: out[i] = __ddiv_rn(a[i], b[i]); break;
+    case 4: out[i] = log_nb(a[i]); break;
+    case 5: out[i] = log(a[i]); break;
+    case 6: out[i] = sqrt_nb(a[i]); break;
+    default: out[i] = __dsqrt_rn(a[i]); break;
   }
 }
 

@@ -229,7 +229,8 @@ def test_lstsq_vs_numpy(k, J):
 
 
 def test_branch_free_math_is_bit_identical():
-    """exp_nb / div_nb (brm_rng.cuh) return CUDA's exp / __ddiv_rn bits on the walker's ranges."""
+    """exp_nb / div_nb / log_nb / sqrt_nb (brm_rng.cuh) return the bits of CUDA's exp / __ddiv_rn / log /
+    __dsqrt_rn on the walker's ranges."""
     from paper_0805_1827_b200 import _native as N
     rng = np.random.default_rng(11)
     n = 1 << 22
@@ -249,6 +250,12 @@ def test_branch_free_math_is_bit_identical():
     a = np.concatenate([num, rng.normal(size=n) * np.exp(rng.uniform(-300, 300, n))])
     b = np.concatenate([den, rng.normal(size=n) * np.exp(rng.uniform(-300, 300, n))])
     assert np.array_equal(run(2, a, b).view(np.int64), run(3, a, b).view(np.int64))
+    # log / sqrt of the AS241 tail: log of u or 1-u in [2^-54, 0.075], sqrt of -log in [2.5, 37.5]
+    u = np.concatenate([rng.uniform(0, 0.075, n), np.exp(rng.uniform(np.log(2.0 ** -54), np.log(0.075), n)),
+                        np.array([2.0 ** -54, 0.075, 0.5, 1.0, 1.5, 2.0 ** 500, np.sqrt(0.5), np.sqrt(2.0)])])
+    assert np.array_equal(run(4, u).view(np.int64), run(5, u).view(np.int64))
+    s = np.concatenate([rng.uniform(2.5, 37.5, n), np.exp(rng.uniform(-600, 600, n))])
+    assert np.array_equal(run(6, s).view(np.int64), run(7, s).view(np.int64))
 
 
 def test_fast_mode_adaboost_deterministic_and_equivalent():
