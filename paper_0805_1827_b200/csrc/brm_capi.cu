@@ -497,8 +497,6 @@ int ctx_create_impl(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t 
       bound[m] = 4.0 * (double)(nfeat + 4) * std::ldexp(1.0, -53) + 1e-300;
     }
   }
-  h.o_thr = put(thr, 1);
-  h.o_ap = put(ap, 1);
   for (int m = 0; m <= nd && capacity == 0; ++m) {
     const int t0 = rl->kind == BRM_RULE_CMC ? starts[m] : 0, cnt = rl->kind == BRM_RULE_CMC ? counts[m] : 0;
     double absum = rl->kind == BRM_RULE_CMC ? std::fabs(icept[m]) : 0.0;
@@ -536,10 +534,17 @@ int ctx_create_impl(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t 
     for (int t = t0; t < t0 + cnt; ++t) absum += std::fabs(ap[t]);
     bound[m] = 4.0 * (double)(cnt + nfeat + 4) * std::ldexp(absum, -53) + 1e-300;
   }
+  h.o_bound = put(bound, nd + 1);
+  // cold region (kernels read it from global memory): the stumps in stump
+  // order for the exact fallback, and the step tables the CTAs index at start
+  h.n_hot = (int)dbl.size();
+  h.o_thr = put(thr, 1);
+  h.o_ap = put(ap, 1);
   h.o_tt = put(tt, 1);
   h.o_tv = put(tv, 1);
-  h.o_bound = put(bound, nd + 1);
   h.n_dbl = (int)dbl.size();
+  // compact (threshold, table value) entries: u_f + 2 per (date, feature)
+  h.n_tab = rl->kind == BRM_RULE_CMC ? (capacity > 0 ? (nd + 1) * capacity : ns) + 2 * (nd + 1) * nfeat + 3 : 0;
   std::vector<int32_t> ints;
   auto puti = [&](const std::vector<int32_t> &v, size_t min_len) {
     int off = (int)ints.size();

@@ -15,12 +15,18 @@ rule, _ = E.build_cmc_rule(p, s, E.CmcBuildConfig(cfg["n_train"], cfg["n_label"]
 mp = pack_market(p, s)
 rp = rule.pack()
 from paper_0805_1827_b200 import _native as N
-N.profile_reset()
-t0 = time.perf_counter()
-G.cmc_calc(mp, rp, 1, 1827, 0, cfg["n_train"], cfg["n_label"], bridge_scalars(p, s, 1), mode=mode)
-t1 = time.perf_counter()
-s_lab = N.profile_read()["walk"][2]
-G.price_blocks(mp, rp, 1 << 22, 1827, mode=mode)
-t2 = time.perf_counter()
-s_all = N.profile_read()["walk"][2]
-print(f"labels(date1) {1e3*(t1-t0):.2f} ms  pricing(2^22) {1e3*(t2-t1):.2f} ms  path-steps: labels {s_lab} pricing {s_all - s_lab}")
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+best = [1e9, 1e9]
+for _ in range(reps):
+    N.profile_reset()
+    N.profile_enable(True)
+    G.cmc_calc(mp, rp, 1, 1827, 0, cfg["n_train"], cfg["n_label"], bridge_scalars(p, s, 1), mode=mode)
+    pr = N.profile_read()
+    s_lab, ms_lab = pr["walk"][2], pr["walk"][0]
+    G.price_blocks(mp, rp, 1 << 22, 1827, mode=mode)
+    pr = N.profile_read()
+    N.profile_enable(False)
+    s_all, ms_all = pr["walk"][2], pr["walk"][0]
+    best = [min(best[0], ms_lab), min(best[1], ms_all - ms_lab)]
+print(f"{mode}: walker labels(date1) {best[0]:.2f} ms  pricing(2^22) {best[1]:.2f} ms  (best of {reps})  "
+      f"path-steps: labels {s_lab} pricing {s_all - s_lab}")
