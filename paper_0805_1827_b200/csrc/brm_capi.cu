@@ -554,6 +554,7 @@ int ctx_create_impl(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t 
   };
   h.o_starts = puti(starts, nd + 1);
   h.o_counts = puti(counts, nd + 1);
+  h.n_int_hot = (int)ints.size();  // feat and the table offsets stay in global memory
   h.o_feat = puti(feat, 1);
   h.o_toff = puti(toff, 1);
   h.o_tcnt = puti(tcnt, 1);

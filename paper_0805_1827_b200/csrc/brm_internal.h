@@ -12,7 +12,7 @@ namespace brm {
 constexpr int kWalkThreads = 256;   // threads per walker CTA
 constexpr int kPathBlock = 4096;    // pricer.py:32 PATH_BLOCK (stream convention)
 constexpr int kPriceChunk = 1024;   // paths per pricing work item (4 per block)
-constexpr int kMaxChunk = 4096;     // largest chunk a walker CTA folds in smem
+constexpr int kMaxChunk = 2048;     // largest chunk a walker CTA folds in smem
 
 struct WalkParams {
   ModelHdr hdr;
