@@ -134,7 +134,10 @@ int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t star
 
 /* Self-test of the walker's branch-free fp64 exp / divide / log / sqrt against
  * CUDA's exp / __ddiv_rn / log / __dsqrt_rn (kind 0 exp_nb(a), 1 exp(a),
- * 2 div_nb(a, b), 3 a / b, 4 log_nb(a), 5 log(a), 6 sqrt_nb(a), 7 sqrt(a)). */
+ * 2 div_nb(a, b), 3 a / b, 4 log_nb(a), 5 log(a), 6 sqrt_nb(a), 7 sqrt(a)),
+ * and of AdaBoost's warp-parallel cumsum against the sequential one (kind 8:
+ * out = np.cumsum order of a[0..n) by one thread, 9: by the warp's binade
+ * tiles; a >= 0). */
 int brm_selftest_math(int32_t device, int32_t kind, const double *a, const double *b, int64_t n, double *out);
 
 /* ---- Path walker ------------------------------------------------------- */

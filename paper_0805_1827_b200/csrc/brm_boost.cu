@@ -34,6 +34,7 @@
 
 #include "../../include/bermuda_b200.h"
 #include "brm_internal.h"
+#include "brm_chain.cuh"
 #include "brm_rng.cuh"
 
 namespace cg = cooperative_groups;
@@ -323,10 +324,12 @@ __device__ __forceinline__ bool cand_less(const Cand &a, const Cand &b) {
 }
 
 // Sequential prefix sums out[k] = in[0] + ... + in[k] continuing from acc
-// (one thread).  Ping-pong over two register chunks: chunk A is summed while
+// (one thread; element k stored at chain_pos<PAD>(k)).  Ping-pong over two
+// register chunks: chunk A is summed while
 // chunk B's shared-memory loads are in flight, then the reverse, so no load
 // latency is exposed (tools/micro_cuda/chain.cu: 9.2 cycles/element vs 13.4
 // for the plain loop unrolled by 8).
+template <bool PAD>
 __device__ __forceinline__ void serial_chain(const double *__restrict__ in, double *__restrict__ out, int cnt,
                                              double &acc) {
   constexpr int C = 16;
@@ -334,30 +337,43 @@ __device__ __forceinline__ void serial_chain(const double *__restrict__ in, doub
   double a[C], b[C];
   if (cnt >= 2 * C) {
 #pragma unroll
-    for (int j = 0; j < C; ++j) a[j] = in[j];
+    for (int j = 0; j < C; ++j) a[j] = in[chain_pos<PAD>(j)];
   }
   for (; k + 2 * C <= cnt; k += 2 * C) {
 #pragma unroll
-    for (int j = 0; j < C; ++j) b[j] = in[k + C + j];
+    for (int j = 0; j < C; ++j) b[j] = in[chain_pos<PAD>(k + C + j)];
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       acc = __dadd_rn(acc, a[j]);
-      out[k + j] = acc;
+      out[chain_pos<PAD>(k + j)] = acc;
     }
     const bool more = k + 4 * C <= cnt;
 #pragma unroll
-    for (int j = 0; j < C; ++j) a[j] = more ? in[k + 2 * C + j] : 0.0;
+    for (int j = 0; j < C; ++j) a[j] = more ? in[chain_pos<PAD>(k + 2 * C + j)] : 0.0;
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       acc = __dadd_rn(acc, b[j]);
-      out[k + C + j] = acc;
+      out[chain_pos<PAD>(k + C + j)] = acc;
     }
   }
   for (; k < cnt; ++k) {
-    acc = __dadd_rn(acc, in[k]);
-    out[k] = acc;
+    acc = __dadd_rn(acc, in[chain_pos<PAD>(k)]);
+    out[chain_pos<PAD>(k)] = acc;
   }
 }
+
+// Chain self-test (brm_selftest_math kinds 8 / 9): the prefix sums of a[0..n)
+// by the one-thread sequential chain and by the warp's binade tiles.
+__global__ void chain_selftest(int kind, const double *a, int64_t n, double *out) {
+  double acc = 0.0;
+  if (kind == 8) {
+    if (threadIdx.x == 0) serial_chain<false>(a, out, (int)n, acc);
+  } else {
+    warp_chain<false>(a, out, (int)n, acc);
+  }
+}
+
+void *chain_selftest_kernel() { return (void *)&chain_selftest; }
 
 __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
   cg::grid_group grid = cg::this_grid();
@@ -435,18 +451,21 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
       double pacc = 0.0, nacc = 0.0;  // np.cumsum(where(y>0, w, 0)): zeros never change a partial sum
       // tiles: all threads gather, the two highest warps run the two sequential
       // chains (the issue arbiter favours high warp ids), all threads write back
-      const int chain_p = blockDim.x - 64, chain_n = blockDim.x - 32;
+      const int wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
       for (int t0 = 0; t0 < max(n_pos, n_neg); t0 += kTile) {
         const int tp = max(0, min(kTile, n_pos - t0)), tn = max(0, min(kTile, n_neg - t0));
         gather_tile(wn, pid + t0, tp, s_in_p);
         gather_tile(wn, nid + t0, tn, s_in_n);
         __syncthreads();
-        if (threadIdx.x == chain_p) {
+        // one thread per chain: the dependent fp64 add (~9 cycles per element)
+        // beats warp_chain's binade tiles on a single warp (brm_chain.cuh)
+        if (threadIdx.x == (nwarp - 2) * 32) {
           const long long c0 = timed ? clock64() : 0;
-          serial_chain(s_in_p, s_out_p, tp, pacc);
+          serial_chain<false>(s_in_p, s_out_p, tp, pacc);
           if (timed) tacc[7] += clock64() - c0;
+        } else if (threadIdx.x == (nwarp - 1) * 32) {
+          serial_chain<false>(s_in_n, s_out_n, tn, nacc);
         }
-        else if (threadIdx.x == chain_n) serial_chain(s_in_n, s_out_n, tn, nacc);
         __syncthreads();
         for (int j = threadIdx.x; j < tp; j += blockDim.x) pc[t0 + j] = s_out_p[j];
         for (int j = threadIdx.x; j < tn; j += blockDim.x) nc[t0 + j] = s_out_n[j];

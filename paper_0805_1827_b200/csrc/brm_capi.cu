@@ -738,7 +738,8 @@ int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t star
 
 int brm_selftest_math(int32_t device, int32_t kind, const double *a, const double *b, int64_t n, double *out) {
   if (n <= 0) return BRM_OK;
-  if (kind < 0 || kind > 7) return fail(BRM_EINVAL, "unknown self-test %d", kind);
+  if (kind < 0 || kind > 9) return fail(BRM_EINVAL, "unknown self-test %d", kind);
+  if (kind >= 8 && n > 2147483647LL) return fail(BRM_EINVAL, "chain self-test too long");
   DeviceScope scope(device);
   Call call(nullptr);
   const double *da, *db = nullptr;
@@ -747,7 +748,12 @@ int brm_selftest_math(int32_t device, int32_t kind, const double *a, const doubl
   if (kind == 2 || kind == 3) BRM_TRY(call.in(b, n, &db));
   BRM_TRY(call.out(out, n, &o));
   void *args[] = {&kind, &da, &db, &n, &o};
-  BRM_CUDA(cudaLaunchKernel(math_selftest_kernel(), dim3((unsigned)((n + 255) / 256)), dim3(256), args, 0, call.stream));
+  if (kind >= 8) {
+    void *cargs[] = {&kind, &da, &n, &o};
+    BRM_CUDA(cudaLaunchKernel(chain_selftest_kernel(), dim3(1), dim3(32), cargs, 0, call.stream));
+  } else {
+    BRM_CUDA(cudaLaunchKernel(math_selftest_kernel(), dim3((unsigned)((n + 255) / 256)), dim3(256), args, 0, call.stream));
+  }
   return call.finish();
 }
 

@@ -258,6 +258,38 @@ def test_branch_free_math_is_bit_identical():
     assert np.array_equal(run(6, s).view(np.int64), run(7, s).view(np.int64))
 
 
+def test_warp_chain_is_bit_identical_to_sequential_cumsum():
+    """AdaBoost's warp-parallel binade-tile prefix sums (brm_chain.cuh) equal the one-thread
+    sequential np.cumsum chain bit for bit: AdaBoost-like weights, wide dynamic ranges, zeros,
+    exact ties (dyadic weights), long and short chains."""
+    from paper_0805_1827_b200 import _native as N
+    rng = np.random.default_rng(23)
+
+    def run(kind, a):
+        out = np.empty(a.size)
+        N.check(N.lib.brm_selftest_math(0, kind, N.ptr(a), N.ptr(None), a.size, N.ptr(out)))
+        return out
+
+    cases = []
+    for n in (1, 2, 31, 257, 1000, 9900, 20000):
+        w = rng.random(n) * np.exp(rng.normal(scale=2.0, size=n))
+        cases.append(w / w.sum())
+    w = np.exp(rng.uniform(-60, 0, 12000))
+    cases.append(w)
+    w = rng.integers(0, 64, 8000).astype(float) * 2.0 ** -20      # dyadic: many exact ties
+    cases.append(w)
+    w = np.where(rng.random(8000) < 0.3, 0.0, rng.random(8000))   # zeros
+    cases.append(w)
+    w = np.concatenate([np.full(100, 1e-300), rng.random(3000), np.full(50, 5e-324)])  # tiny and subnormal
+    cases.append(w)
+    cases.append(np.sort(rng.random(5000))[::-1].copy())           # decreasing
+    for a in cases:
+        a = np.ascontiguousarray(a)
+        seq, war = run(8, a), run(9, a)
+        assert np.array_equal(seq.view(np.int64), war.view(np.int64)), a.size
+        assert np.array_equal(seq, np.cumsum(a))
+
+
 def test_fast_mode_adaboost_deterministic_and_equivalent():
     """Fixed-point fast fit: deterministic, same first stump as the exact fit on a clear split,
     training error within 1% of the exact fit."""
