@@ -585,6 +585,10 @@ int ctx_create_impl(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t 
     brm_ctx_destroy(c);
     return fail(e == cudaErrorMemoryAllocation ? BRM_ENOMEM : BRM_ECUDA, "context upload: %s", cudaGetErrorString(e));
   }
+  if (h.n_tab > 65535) {
+    brm_ctx_destroy(c);
+    return fail(BRM_EINVAL, "too many stumps (%d step-table entries, at most 65535)", h.n_tab);
+  }
   if (smem_model(c) + 8 * 64 > c->info.max_smem) {
     brm_ctx_destroy(c);
     return fail(BRM_EINVAL, "model image (%d B) exceeds shared memory", smem_model(c));
