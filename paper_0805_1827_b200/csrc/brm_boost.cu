@@ -293,7 +293,7 @@ __device__ __forceinline__ void gather_tile(const double *__restrict__ w, const 
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int j = threadIdx.x + g * kBoostThreads;
-    if (j < cnt) s[j] = v[g];
+    if (j < cnt) s[chain_pos<true>(j)] = v[g];  // warp_chain's padded layout
   }
 }
 
@@ -323,51 +323,12 @@ __device__ __forceinline__ bool cand_less(const Cand &a, const Cand &b) {
   return a.err < b.err || (a.err == b.err && a.key < b.key);
 }
 
-// Sequential prefix sums out[k] = in[0] + ... + in[k] continuing from acc
-// (one thread; element k stored at chain_pos<PAD>(k)).  Ping-pong over two
-// register chunks: chunk A is summed while
-// chunk B's shared-memory loads are in flight, then the reverse, so no load
-// latency is exposed (tools/micro_cuda/chain.cu: 9.2 cycles/element vs 13.4
-// for the plain loop unrolled by 8).
-template <bool PAD>
-__device__ __forceinline__ void serial_chain(const double *__restrict__ in, double *__restrict__ out, int cnt,
-                                             double &acc) {
-  constexpr int C = 16;
-  int k = 0;
-  double a[C], b[C];
-  if (cnt >= 2 * C) {
-#pragma unroll
-    for (int j = 0; j < C; ++j) a[j] = in[chain_pos<PAD>(j)];
-  }
-  for (; k + 2 * C <= cnt; k += 2 * C) {
-#pragma unroll
-    for (int j = 0; j < C; ++j) b[j] = in[chain_pos<PAD>(k + C + j)];
-#pragma unroll
-    for (int j = 0; j < C; ++j) {
-      acc = __dadd_rn(acc, a[j]);
-      out[chain_pos<PAD>(k + j)] = acc;
-    }
-    const bool more = k + 4 * C <= cnt;
-#pragma unroll
-    for (int j = 0; j < C; ++j) a[j] = more ? in[chain_pos<PAD>(k + 2 * C + j)] : 0.0;
-#pragma unroll
-    for (int j = 0; j < C; ++j) {
-      acc = __dadd_rn(acc, b[j]);
-      out[chain_pos<PAD>(k + C + j)] = acc;
-    }
-  }
-  for (; k < cnt; ++k) {
-    acc = __dadd_rn(acc, in[chain_pos<PAD>(k)]);
-    out[chain_pos<PAD>(k)] = acc;
-  }
-}
-
 // Chain self-test (brm_selftest_math kinds 8 / 9): the prefix sums of a[0..n)
 // by the one-thread sequential chain and by the warp's binade tiles.
 __global__ void chain_selftest(int kind, const double *a, int64_t n, double *out) {
   double acc = 0.0;
   if (kind == 8) {
-    if (threadIdx.x == 0) serial_chain<false>(a, out, (int)n, acc);
+    if (threadIdx.x == 0) serial_chain<false>(a, out, 0, (int)n, acc);
   } else {
     warp_chain<false>(a, out, (int)n, acc);
   }
@@ -380,10 +341,11 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *s_node = reinterpret_cast<double *>(smem_raw);               // [L + I]
   double *s_in_p = s_node + 2 * P.n_leaves;
-  double *s_in_n = s_in_p + kTile;
-  double *s_out_p = s_in_n + kTile;
-  double *s_out_n = s_out_p + kTile;
-  unsigned char *s_after = reinterpret_cast<unsigned char *>(s_out_n + kTile);
+  constexpr int kTileP = chain_padded_len(kTile);  // padded tiles (chain_pos)
+  double *s_in_n = s_in_p + kTileP;
+  double *s_out_p = s_in_n + kTileP;
+  double *s_out_n = s_out_p + kTileP;
+  unsigned char *s_after = reinterpret_cast<unsigned char *>(s_out_n + kTileP);
   __shared__ Cand s_cand[kBoostThreads / 32];
   __shared__ int s_stop;
   __shared__ double s_alpha, s_thr, s_pol, s_err;
@@ -457,18 +419,18 @@ __global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
         gather_tile(wn, pid + t0, tp, s_in_p);
         gather_tile(wn, nid + t0, tn, s_in_n);
         __syncthreads();
-        // one thread per chain: the dependent fp64 add (~9 cycles per element)
-        // beats warp_chain's binade tiles on a single warp (brm_chain.cuh)
-        if (threadIdx.x == (nwarp - 2) * 32) {
+        // one warp per chain: binade tiles (brm_chain.cuh), ~2x the sequential
+        // fp64 add chain's 9 cycles per element
+        if (wid == nwarp - 2) {
           const long long c0 = timed ? clock64() : 0;
-          serial_chain<false>(s_in_p, s_out_p, tp, pacc);
+          warp_chain<true, 32>(s_in_p, s_out_p, tp, pacc);
           if (timed) tacc[7] += clock64() - c0;
-        } else if (threadIdx.x == (nwarp - 1) * 32) {
-          serial_chain<false>(s_in_n, s_out_n, tn, nacc);
+        } else if (wid == nwarp - 1) {
+          warp_chain<true, 32>(s_in_n, s_out_n, tn, nacc);
         }
         __syncthreads();
-        for (int j = threadIdx.x; j < tp; j += blockDim.x) pc[t0 + j] = s_out_p[j];
-        for (int j = threadIdx.x; j < tn; j += blockDim.x) nc[t0 + j] = s_out_n[j];
+        for (int j = threadIdx.x; j < tp; j += blockDim.x) pc[t0 + j] = s_out_p[chain_pos<true>(j)];
+        for (int j = threadIdx.x; j < tn; j += blockDim.x) nc[t0 + j] = s_out_n[chain_pos<true>(j)];
       }
       __syncthreads();
     BRM_TSLOT(2);
@@ -1214,7 +1176,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       const size_t smem_cap = (size_t)smem_max - 2048;  // static shared arrays of the kernel
       const size_t tree_bytes = sizeof(int2) * (tree.leaves.size() + tree.children.size()) +
                                 sizeof(int) * tree.level_end.size();
-      size_t smem = sizeof(double) * (2 * tree.leaves.size() + 4 * kTile);
+      size_t smem = sizeof(double) * (2 * tree.leaves.size() + 4 * chain_padded_len(kTile));
       P.tree_smem = smem + tree_bytes <= smem_cap ? 1 : 0;
       if (P.tree_smem) smem += tree_bytes;
       void *boost_fn = (void *)boost_kernel;

@@ -27,7 +27,7 @@ __global__ void k_warp(const double *g, double *o, int n, long long *cyc) {
   __syncthreads();
   long long t0 = clock64();
   double acc = 0.0;
-  if (threadIdx.x < 32) warp_chain<true>(in, out, n, acc);
+  if (threadIdx.x < 32) warp_chain<true, CHAIN_T>(in, out, n, acc);
   __syncthreads();
   if (threadIdx.x == 0) cyc[0] = clock64() - t0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) o[i] = out[chain_pos<true>(i)];
