@@ -97,7 +97,7 @@ __device__ __forceinline__ void serial_chain(const double *__restrict__ in, doub
   }
 }
 
-constexpr int kChainLead = 512;  // leading elements summed one by one (binade crossings are dense there)
+constexpr int kChainLead = 256;  // leading elements summed one by one (binade crossings are dense there)
 
 // out[k] = acc + in[0] + ... + in[k] in sequential fp64 order, k < cnt, for
 // in[] >= 0 (finite); element k stored at chain_pos<PAD>(k).  Called by all

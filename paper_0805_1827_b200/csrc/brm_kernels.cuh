@@ -23,7 +23,7 @@ namespace brm {
 
 // ---------------------------------------------------------------- walk ----
 template <int D, bool FAST>
-__global__ void __launch_bounds__(kWalkThreads, FAST ? 3 : 2) walk_units(WalkParams P) {
+__global__ void __launch_bounds__(kWalkThreads, (FAST && D < 20) ? 3 : 2) walk_units(WalkParams P) {
   constexpr int TG = FAST ? 1 : TailGroup<D>::G;
   __shared__ double s_tq_buf[(kWalkThreads / 32) * 32 * TG];
   __shared__ unsigned short s_tq_idx[(kWalkThreads / 32) * 32 * TG];

@@ -1,5 +1,8 @@
-"""C5 walker launches for ncu: build the real C5 rule, then one label launch (date 1) and one
-pricing launch (2^22 paths).  ncu -k regex:walk_units -s 8 -c 2 profiles the last two."""
+"""Walker launches of a CMC config for ncu: build the real rule, then one label launch (date 1)
+and one pricing launch (2^22 paths).  ncu -k regex:walk_units -s 8 -c 2 profiles the last two
+(C5; use -s <n_dates - 1> for other configs).
+
+usage: python tools/prof_c5.py [parity|fast] [reps] [config]"""
 import sys, time
 sys.path.insert(0, '.')
 import numpy as np
@@ -9,9 +12,10 @@ from paper_0805_1827_b200 import backend as G
 from paper_0805_1827_b200.boundary_cmc import bridge_scalars
 from paper_0805_1827_b200.packs import pack_market
 mode = sys.argv[1] if len(sys.argv) > 1 else "parity"
-cfg = bench.CONFIGS["c5"]
+cfg = bench.CONFIGS[sys.argv[3] if len(sys.argv) > 3 else "c5"]
 p, s = bench.build_objects(cfg, E)
-rule, _ = E.build_cmc_rule(p, s, E.CmcBuildConfig(cfg["n_train"], cfg["n_label"], cfg["rounds"]), seed=1827, mode=mode)
+rule, _ = E.build_cmc_rule(p, s, E.CmcBuildConfig(cfg["n_train"], cfg["n_label"], cfg["rounds"]), seed=1827,
+                           sampler=cfg["sampler"], mode=mode)
 mp = pack_market(p, s)
 rp = rule.pack()
 from paper_0805_1827_b200 import _native as N
@@ -20,7 +24,8 @@ best = [1e9, 1e9]
 for _ in range(reps):
     N.profile_reset()
     N.profile_enable(True)
-    G.cmc_calc(mp, rp, 1, 1827, 0, cfg["n_train"], cfg["n_label"], bridge_scalars(p, s, 1), mode=mode)
+    G.cmc_calc(mp, rp, 1, 1827, 0, cfg["n_train"], cfg["n_label"], bridge_scalars(p, s, 1), cfg["sampler"],
+               mode=mode)
     pr = N.profile_read()
     s_lab, ms_lab = pr["walk"][2], pr["walk"][0]
     G.price_blocks(mp, rp, 1 << 22, 1827, mode=mode)
