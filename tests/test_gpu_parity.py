@@ -179,9 +179,11 @@ def test_sampler_forward_vs_oracle():
     assert np.max(np.abs(g / xs - 1.0)) <= 1e-14
 
 
-def test_fast_mode_statistical():
-    """fp32 Box-Muller mode: price within 4 combined SE of the fp64 oracle."""
-    (p, s), rp = CASES["maxcall5_cmc"]()
+@pytest.mark.parametrize("case", ["maxcall5_cmc", "basket40_cmc"])
+def test_fast_mode_statistical(case):
+    """fp32 Box-Muller mode: price within 4 combined SE of the fp64 parity walker (d=40: the
+    correlated factor and the shared-memory path state of the large-d fast walker)."""
+    (p, s), rp = CASES[case]()
     mp = CS.packs(p, s)
     n = 1 << 18
     g = G.price_blocks(mp, rp, n, 1827, mode="fast")
