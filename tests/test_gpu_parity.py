@@ -97,6 +97,35 @@ def test_decisions_bit_exact():
             assert np.array_equal(g, o), (key, m)
 
 
+def test_decisions_bucket_overflow_and_edge_thresholds():
+    """Step-table lookups where buckets hold many thresholds (clustered within one key, so the
+    date takes the bucket-scan path), thresholds at -inf (all-constant majority stumps), ties
+    between a state and a threshold, and states far outside the thresholds' key range: decisions
+    equal the oracle's stump-order sum bit for bit."""
+    from paper_0805_1827_b200.packs import RulePack
+    p, s = CS.maxcall(5)
+    mp = CS.packs(p, s)
+    rng = np.random.default_rng(12)
+    per = {}
+    for m in range(1, s.n_dates):
+        n = 60
+        feat = rng.integers(0, 6, n)
+        thr = np.where(rng.random(n) < 0.5, 100.0 * (1 + 1e-12 * rng.integers(0, 50, n)),  # one key
+                       rng.uniform(60, 160, n))
+        thr[:3] = -np.inf
+        per[m] = (feat, thr, rng.choice([-1.0, 1.0], n), rng.uniform(0.05, 1.0, n), rng.normal(scale=0.3))
+    rp = RulePack.from_stumps(s.n_dates, per, True)
+    states = mp.s0 * np.exp(0.3 * rng.normal(size=(3000, p.d)))
+    states[:200] = 100.0 * (1 + 1e-12 * rng.integers(0, 50, (200, p.d)))  # on / between clustered thresholds
+    states[200:220] = 1e-300
+    states[220:240] = 1e300
+    octx = O.Ctx(mp, rp)
+    for m in (1, 4, 7):
+        g = G.decisions(mp, rp, states, m, mode="parity")
+        o = np.array([O.decision(octx, m, x) for x in states])
+        assert np.array_equal(g, o), m
+
+
 def test_cmc_labels_vs_oracle():
     (p, s), rp = CASES["maxcall5_cmc"]()
     mp = CS.packs(p, s)
