@@ -649,6 +649,8 @@ struct FastBoostParams {
   int n, F, rounds, raw;
   const double *xs, *xsorted, *y;
   const int *order;
+  double *ysorted;              // [F][n] labels in each feature's sorted order (filled by the kernel)
+  double *wpart;                // [gridDim] per-slice sums of the new weights (fixed CTA order)
   double *w;                    // [n] fp64 weights (unnormalised between rounds)
   long long *feat_err;          // [F] best integer error of each feature
   int *feat_pos;                // [F]
@@ -677,11 +679,9 @@ __device__ __forceinline__ long long fixw(double w, double inv_s) { return __dou
 
 __global__ void __launch_bounds__(kBoostThreads) boost_fast_kernel(FastBoostParams P) {
   using Scan = cub::BlockScan<long long, kBoostThreads>;
-  using Red = cub::BlockReduce<long long, kBoostThreads>;
   __shared__ typename Scan::TempStorage s_scan;
-  __shared__ typename Red::TempStorage s_redi;
   __shared__ double s_red[kBoostThreads / 32];
-  __shared__ long long s_tot, s_totneg, s_carry_p, s_carry_n;
+  __shared__ long long s_carry_p, s_carry_n;
   __shared__ struct { long long err; int key; } s_cand[kBoostThreads / 32];
   __shared__ int s_stop, s_feat;
   __shared__ double s_thr, s_pol, s_alpha, s_err;
@@ -692,31 +692,38 @@ __global__ void __launch_bounds__(kBoostThreads) boost_fast_kernel(FastBoostPara
   const int n_pos_all = *P.n_pos;
   if (one_class_exit(P.raw, n, n_pos_all, P.out_count, P.out_intercept)) return;
   int count = 0;
+  const int *ord = P.order + (size_t)f * n;
+  const double *xf = P.xsorted + (size_t)f * n;
+  double *ysf = P.ysorted + (size_t)f * n;
+  // labels in this feature's sorted order, once per fit: the split scan then
+  // gathers only the weights
+  for (int i = threadIdx.x; i < n; i += blockDim.x) ysf[i] = P.y[ord[i]];
+  __syncthreads();
   for (int round = 0; round < P.rounds; ++round) {
-    const double ssum = cta_sum_fixed(P.w, n, s_red);
+    // sum of the weights: round 0 by every CTA, later rounds from the slice
+    // sums the previous reweight published (same order in every CTA)
+    double ssum;
+    if (round == 0) {
+      ssum = cta_sum_fixed(P.w, n, s_red);
+    } else {
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(P.wpart + b);
+        s_red[0] = t;
+      }
+      __syncthreads();
+      ssum = s_red[0];
+      __syncthreads();
+    }
     const double inv_s = 1.0 / ssum;
-    // totals (exact)
-    long long tp = 0, tn = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const long long W = fixw(P.w[i], inv_s);
-      if (P.y[i] > 0.0) tp += W;
-      else tn += W;
-    }
-    tp = Red(s_redi).Sum(tp);
+    if (threadIdx.x == 0) s_carry_p = s_carry_n = 0;
     __syncthreads();
-    tn = Red(s_redi).Sum(tn);
-    if (threadIdx.x == 0) {
-      s_tot = tp + tn;
-      s_totneg = tn;
-      s_carry_p = s_carry_n = 0;
-    }
-    __syncthreads();
-    const long long total = s_tot, tot_neg = s_totneg;
-    // split search: one block scan per tile of sorted positions
-    long long best_err = LLONG_MAX;
-    int best_key = INT_MAX;
-    const int *ord = P.order + (size_t)f * n;
-    const double *xf = P.xsorted + (size_t)f * n;
+    // split search: one block scan per tile of sorted positions.  With d_i =
+    // (positives - negatives up to i), err+ = d_i + tot_neg and err- = tot_pos
+    // - d_i, so the argmins need only min / max of d_i; the class totals are
+    // the scan's final carries
+    long long dmin = LLONG_MAX, dmax = LLONG_MIN;
+    int kmin = INT_MAX, kmax = INT_MAX;
     constexpr int ITEMS = 8;  // consecutive sorted positions per thread per tile
     for (int t0 = 0; t0 < n; t0 += ITEMS * blockDim.x) {
       const int i0 = t0 + threadIdx.x * ITEMS;
@@ -726,9 +733,8 @@ __global__ void __launch_bounds__(kBoostThreads) boost_fast_kernel(FastBoostPara
         const int i = i0 + k;
         wp[k] = wn_[k] = 0;
         if (i < n) {
-          const int id = ord[i];
-          const long long W = fixw(P.w[id], inv_s);
-          if (P.y[id] > 0.0) wp[k] = W;
+          const long long W = fixw(P.w[ord[i]], inv_s);
+          if (ysf[i] > 0.0) wp[k] = W;
           else wn_[k] = W;
         }
       }
@@ -746,9 +752,9 @@ __global__ void __launch_bounds__(kBoostThreads) boost_fast_kernel(FastBoostPara
         cp += wp[k];
         cn += wn_[k];
         if (i < n - 1 && __dsub_rn(xf[i + 1], xf[i]) > 0.0) {
-          const long long ep = cp + (tot_neg - cn), em = total - ep;
-          if (ep < best_err || (ep == best_err && 2 * i < best_key)) best_err = ep, best_key = 2 * i;
-          if (em < best_err || (em == best_err && 2 * i + 1 < best_key)) best_err = em, best_key = 2 * i + 1;
+          const long long dd = cp - cn;
+          if (dd < dmin) dmin = dd, kmin = 2 * i;        // positions ascend: first hit keeps the lowest key
+          if (dd > dmax) dmax = dd, kmax = 2 * i + 1;
         }
       }
       __syncthreads();
@@ -758,15 +764,29 @@ __global__ void __launch_bounds__(kBoostThreads) boost_fast_kernel(FastBoostPara
       }
       __syncthreads();
     }
+    const long long tot_pos = s_carry_p, tot_neg = s_carry_n, total = tot_pos + tot_neg;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-      const long long oe = __shfl_down_sync(0xffffffffu, best_err, off);
-      const int ok = __shfl_down_sync(0xffffffffu, best_key, off);
-      if (oe < best_err || (oe == best_err && ok < best_key)) best_err = oe, best_key = ok;
+      const long long o1 = __shfl_down_sync(0xffffffffu, dmin, off), o2 = __shfl_down_sync(0xffffffffu, dmax, off);
+      const int k1 = __shfl_down_sync(0xffffffffu, kmin, off), k2 = __shfl_down_sync(0xffffffffu, kmax, off);
+      if (o1 < dmin || (o1 == dmin && k1 < kmin)) dmin = o1, kmin = k1;
+      if (o2 > dmax || (o2 == dmax && k2 < kmax)) dmax = o2, kmax = k2;
     }
-    if ((threadIdx.x & 31) == 0) s_cand[threadIdx.x >> 5] = {best_err, best_key};
+    if ((threadIdx.x & 31) == 0) {
+      // this warp's best of the two error lists (lowest key at equal error)
+      long long best_err = LLONG_MAX;
+      int best_key = INT_MAX;
+      if (kmin != INT_MAX) best_err = dmin + tot_neg, best_key = kmin;
+      if (kmax != INT_MAX) {
+        const long long em = tot_pos - dmax;
+        if (em < best_err || (em == best_err && kmax < best_key)) best_err = em, best_key = kmax;
+      }
+      s_cand[threadIdx.x >> 5] = {best_err, best_key};
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
+      long long best_err = s_cand[0].err;
+      int best_key = s_cand[0].key;
       for (int w = 1; w < (int)blockDim.x / 32; ++w)
         if (s_cand[w].err < best_err || (s_cand[w].err == best_err && s_cand[w].key < best_key))
           best_err = s_cand[w].err, best_key = s_cand[w].key;
@@ -820,9 +840,21 @@ __global__ void __launch_bounds__(kBoostThreads) boost_fast_kernel(FastBoostPara
       const double a = s_alpha, thr = s_thr, pol = s_pol;
       const int feat = s_feat;
       const double e_agree = exp(-a), e_miss = exp(a);
+      double part = 0.0;
       for (int i = w_lo + threadIdx.x; i < w_hi; i += blockDim.x) {
         const double pred = P.xs[(size_t)i * F + feat] > thr ? pol : -pol;
-        P.w[i] = P.w[i] * inv_s * ((P.y[i] * pred > 0.0) ? e_agree : e_miss);
+        const double wn = P.w[i] * inv_s * ((P.y[i] * pred > 0.0) ? e_agree : e_miss);
+        P.w[i] = wn;
+        part += wn;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) part += __shfl_down_sync(0xffffffffu, part, off);
+      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = part;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)blockDim.x / 32; ++w) t += s_red[w];
+        P.wpart[blockIdx.x] = t;
       }
     }
     grid.sync();
@@ -1194,6 +1226,8 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
         Q.y = d_y;
         Q.order = d_order;
         Q.w = d_w;
+        BCU(S.get(&Q.ysorted, (size_t)F * n));
+        BCU(S.get(&Q.wpart, F));
         long long *d_ferr = nullptr;
         BCU(S.get(&d_ferr, F));
         Q.feat_err = d_ferr;
