@@ -454,10 +454,6 @@ int ctx_create_impl(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t 
   h.o_mu = put(mu, d);
   h.o_vol = put(vol, d);
   h.o_chol = put(chol, (size_t)d * d);
-  std::vector<double> cholT((size_t)d * d);
-  for (int i = 0; i < d; ++i)
-    for (int a = 0; a < d; ++a) cholT[(size_t)a * d + i] = chol[(size_t)i * d + a];
-  h.o_cholT = put(cholT, (size_t)d * d);
   h.o_disc = put(disc, nd + 1);
   h.o_s0 = put(s0, d);
   h.o_izc = put(izc, 1);
