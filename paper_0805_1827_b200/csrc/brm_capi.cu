@@ -1095,7 +1095,8 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   P.hist_offset = P.vals_offset + ((8 * per_cta + 15) & ~15);
   const int smem = P.hist_offset + 8 * (P.max_iter + 1);
   if (smem > c->info.max_smem) return fail(BRM_EINVAL, "probe solve needs %d B of shared memory", smem);
-  BRM_TRY(allow_smem(c->kern.iz, smem));
+  void *kiz = (c->hdr.payoff == BRM_PAY_GEOPUT && !c->fast() && c->kern.iz_geo) ? c->kern.iz_geo : c->kern.iz;
+  BRM_TRY(allow_smem(kiz, smem));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(n * csize));
   cfg.blockDim = dim3(kWalkThreads);
@@ -1111,7 +1112,7 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   void *args[] = {&P};
   {
     const int tok_ = prof_begin(PK_IZ, call.stream);
-    BRM_CUDA(cudaLaunchKernelExC(&cfg, c->kern.iz, args));
+    BRM_CUDA(cudaLaunchKernelExC(&cfg, kiz, args));
     prof_end(tok_, call.stream);
   }
   return call.finish();

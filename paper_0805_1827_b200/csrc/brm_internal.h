@@ -89,6 +89,7 @@ struct SampleParams {
 
 struct KernelTriple {
   void *walk, *iz, *dec;
+  void *iz_geo = nullptr;  // parity I&Z probes specialised for the geometric put (d > 1)
 };
 
 // Kernel families for launch accounting (brm_prof.cu, BRM_PROF_* in the C ABI).

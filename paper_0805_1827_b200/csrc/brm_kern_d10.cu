@@ -4,6 +4,7 @@
 namespace brm {
 KernelTriple kernels_d10(bool fast) {
   if (fast) return KernelTriple{(void *)&walk_units<10, true>, (void *)&iz_probes<10, true>, (void *)&decisions<10, true>};
-  return KernelTriple{(void *)&walk_units<10, false>, (void *)&iz_probes<10, false>, (void *)&decisions<10, false>};
+  return KernelTriple{(void *)&walk_units<10, false>, (void *)&iz_probes<10, false>, (void *)&decisions<10, false>,
+                      (void *)&iz_probes<10, false, true>};
 }
 }  // namespace brm

@@ -4,6 +4,7 @@
 namespace brm {
 KernelTriple kernels_d2(bool fast) {
   if (fast) return KernelTriple{(void *)&walk_units<2, true>, (void *)&iz_probes<2, true>, (void *)&decisions<2, true>};
-  return KernelTriple{(void *)&walk_units<2, false>, (void *)&iz_probes<2, false>, (void *)&decisions<2, false>};
+  return KernelTriple{(void *)&walk_units<2, false>, (void *)&iz_probes<2, false>, (void *)&decisions<2, false>,
+                      (void *)&iz_probes<2, false, true>};
 }
 }  // namespace brm

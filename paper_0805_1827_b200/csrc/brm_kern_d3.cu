@@ -4,6 +4,7 @@
 namespace brm {
 KernelTriple kernels_d3(bool fast) {
   if (fast) return KernelTriple{(void *)&walk_units<3, true>, (void *)&iz_probes<3, true>, (void *)&decisions<3, true>};
-  return KernelTriple{(void *)&walk_units<3, false>, (void *)&iz_probes<3, false>, (void *)&decisions<3, false>};
+  return KernelTriple{(void *)&walk_units<3, false>, (void *)&iz_probes<3, false>, (void *)&decisions<3, false>,
+                      (void *)&iz_probes<3, false, true>};
 }
 }  // namespace brm

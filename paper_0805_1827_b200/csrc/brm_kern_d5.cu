@@ -4,6 +4,7 @@
 namespace brm {
 KernelTriple kernels_d5(bool fast) {
   if (fast) return KernelTriple{(void *)&walk_units<5, true>, (void *)&iz_probes<5, true>, (void *)&decisions<5, true>};
-  return KernelTriple{(void *)&walk_units<5, false>, (void *)&iz_probes<5, false>, (void *)&decisions<5, false>};
+  return KernelTriple{(void *)&walk_units<5, false>, (void *)&iz_probes<5, false>, (void *)&decisions<5, false>,
+                      (void *)&iz_probes<5, false, true>};
 }
 }  // namespace brm

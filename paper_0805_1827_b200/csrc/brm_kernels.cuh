@@ -102,7 +102,9 @@ __device__ inline double probe_state(const ModelHdr &h, const double *seed, int 
   return x;
 }
 
-template <int D, bool FAST>
+// GEOK: the geometric-put instance (walk_paths' GEO step; launched only for
+// that payoff).
+template <int D, bool FAST, bool GEOK = false>
 __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
   constexpr int TG = FAST ? 1 : TailGroup<D>::G;
   __shared__ double s_tq_buf[(kWalkThreads / 32) * 32 * TG];
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
     const uint64_t draw_base = P.solver == 0 ? (uint64_t)it * slab : 0;
     const uint64_t base0 = unit_base<FAST>(draw_base, P.normals != nullptr);
     if (p0 < p1)
-      walk_paths<D, FAST>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, nullptr,
+      walk_paths<D, FAST, GEOK>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, nullptr,
                           nullptr, P.steps, tq);
     __syncthreads();
     double s = 0.0, q = 0.0;

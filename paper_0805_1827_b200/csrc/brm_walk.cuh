@@ -74,7 +74,27 @@ __host__ __device__ __forceinline__ uint64_t unit_base(uint64_t draw_base, bool 
 
 // Walk paths [p0, p1) of one unit from the shared start state.  *s_next must
 // hold p0 + blockDim.x (set by the caller, followed by __syncthreads()).
-template <int D, bool FAST>
+// Geometric put in fp64 (GEO kernels): the step's log prices, formed once
+// with the straight-line log (CUDA's log bits for the positive normal prices
+// a walk produces), feed both the geometric mean -- the same sequential sum,
+// divide and exp as aggregate() -- and a log-space I&Z surface.
+template <int D>
+__device__ __forceinline__ double geo_payoff(const Model<double> &M, const double *v, double &agg, double *lv) {
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    lv[i] = (v[i] >= 0x1p-1022 && v[i] < 0x1p1023) ? log_nb(v[i]) : log(v[i]);
+    s = __dadd_rn(s, lv[i]);
+  }
+  agg = exp_nb(__ddiv_rn(s, (double)D));
+  const double p = __dsub_rn(M.strike, agg);
+  return p > 0.0 ? p : 0.0;
+}
+
+// GEO: the geometric-put walker (geo_payoff; only launched for that payoff).
+// Kept out of the generic instances: code a kernel never runs still costs
+// registers and instruction cache on the max-call path.
+template <int D, bool FAST, bool GEO = false>
 __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_start, int m_start, int n_steps,
                            uint64_t key, uint64_t stream, uint64_t base0, int p0, int p1, const NormalSrc &ns,
                            double *vals, int *s_next, double *path_out, int32_t *stop_out,
@@ -115,8 +135,18 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
       }
       const int m = m_start + k + 1;
       R agg;
-      const R pay = payoff_agg<D>(M, v, agg);
-      if (pay > (R)0 && rule_stop<D>(M, m, v, agg)) {
+      bool stop;
+      R pay;
+      if constexpr (GEO && !FAST && D > 1) {
+        R lv[D > 1 ? D : 1];
+        pay = geo_payoff<D>(M, v, agg, lv);
+        stop = pay > (R)0 && (m == M.n_dates || (M.rule == RULE_IZ ? iz_stop<D>(M, m, v, lv)
+                                                                  : rule_stop<D>(M, m, v, agg)));
+      } else {
+        pay = payoff_agg<D>(M, v, agg);
+        stop = pay > (R)0 && rule_stop<D>(M, m, v, agg);
+      }
+      if (stop) {
         val = (double)pay * M.disc[m - m_start];
         stop_m = m;
         done = true;
