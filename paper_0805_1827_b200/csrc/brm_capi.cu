@@ -299,15 +299,18 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   const int smem = P.vals_offset + 8 * P.chunk;
   if (smem > c->info.max_smem) return fail(BRM_EINVAL, "model image too large for shared memory (%d B)", smem);
   BRM_TRY(call.scratch<double>(2 * (size_t)P.n_items, &P.partials));
-  BRM_TRY(allow_smem(c->kern.walk, smem));
+  void *kwalk = (c->hdr.payoff == BRM_PAY_MAXCALL && c->hdr.rule == BRM_RULE_CMC && c->kern.walk_mc && !P.normals)
+                    ? c->kern.walk_mc
+                    : c->kern.walk;
+  BRM_TRY(allow_smem(kwalk, smem));
   int per_sm = 0;
-  BRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->kern.walk, kWalkThreads, smem));
+  BRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kwalk, kWalkThreads, smem));
   if (per_sm < 1) return fail(BRM_EINVAL, "walker does not fit on an SM (smem %d B)", smem);
   const int grid = std::min(P.n_items, per_sm * c->info.sms);
   void *args[] = {&P};
   {
     const int tok_ = prof_begin(PK_WALK, call.stream);
-    BRM_CUDA(cudaLaunchKernel(c->kern.walk, dim3(grid), dim3(kWalkThreads), args, smem, call.stream));
+    BRM_CUDA(cudaLaunchKernel(kwalk, dim3(grid), dim3(kWalkThreads), args, smem, call.stream));
     prof_end(tok_, call.stream);
   }
   FinishParams F{};

@@ -3,8 +3,10 @@
 
 namespace brm {
 KernelTriple kernels_d10(bool fast) {
-  if (fast) return KernelTriple{(void *)&walk_units<10, true>, (void *)&iz_probes<10, true>, (void *)&decisions<10, true>};
+  if (fast)
+    return KernelTriple{(void *)&walk_units<10, true>, (void *)&iz_probes<10, true>, (void *)&decisions<10, true>,
+                        nullptr, (void *)&walk_units<10, true, WALK_MAXCALL_CMC>};
   return KernelTriple{(void *)&walk_units<10, false>, (void *)&iz_probes<10, false>, (void *)&decisions<10, false>,
-                      (void *)&iz_probes<10, false, true>};
+                      (void *)&iz_probes<10, false, true>, (void *)&walk_units<10, false, WALK_MAXCALL_CMC>};
 }
 }  // namespace brm

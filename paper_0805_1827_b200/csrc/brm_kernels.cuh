@@ -22,7 +22,7 @@ namespace cg = cooperative_groups;
 namespace brm {
 
 // ---------------------------------------------------------------- walk ----
-template <int D, bool FAST>
+template <int D, bool FAST, int SPEC = WALK_GENERIC>
 __global__ void __launch_bounds__(kWalkThreads, (FAST && D < 20) ? 3 : 2) walk_units(WalkParams P) {
   constexpr int TG = FAST ? 1 : TailGroup<D>::G;
   __shared__ double s_tq_buf[(kWalkThreads / 32) * 32 * TG];
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kWalkThreads, (FAST && D < 20) ? 3 : 2) walk_u
       const uint64_t base0 = unit_base<FAST>(P.draw_base, P.normals != nullptr);
       double *pout = P.path_out ? P.path_out + (size_t)u * P.per_unit : nullptr;
       int32_t *sout = P.stop_out ? P.stop_out + (size_t)u * P.per_unit : nullptr;
-      walk_paths<D, FAST>(M, s_start, P.m_start, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, pout,
+      walk_paths<D, FAST, SPEC>(M, s_start, P.m_start, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, pout,
                           sout, P.steps, tq);
     }
     __syncthreads();
@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
     const uint64_t draw_base = P.solver == 0 ? (uint64_t)it * slab : 0;
     const uint64_t base0 = unit_base<FAST>(draw_base, P.normals != nullptr);
     if (p0 < p1)
-      walk_paths<D, FAST, GEOK>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, nullptr,
+      walk_paths<D, FAST, GEOK ? WALK_GEO : WALK_GENERIC>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1, ns,
+                                                          vals, &s_next, nullptr,
                           nullptr, P.steps, tq);
     __syncthreads();
     double s = 0.0, q = 0.0;

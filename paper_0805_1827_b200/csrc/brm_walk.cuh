@@ -91,10 +91,13 @@ __device__ __forceinline__ double geo_payoff(const Model<double> &M, const doubl
   return p > 0.0 ? p : 0.0;
 }
 
-// GEO: the geometric-put walker (geo_payoff; only launched for that payoff).
-// Kept out of the generic instances: code a kernel never runs still costs
-// registers and instruction cache on the max-call path.
-template <int D, bool FAST, bool GEO = false>
+// Specialised steps (each instance launched only for its payoff / rule; code
+// a kernel never runs still costs registers and instruction cache):
+// WALK_GEO: the geometric put (geo_payoff); WALK_MAXCALL_CMC: the max-call
+// payoff under a CMC rule.
+enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_MAXCALL_CMC = 2 };
+
+template <int D, bool FAST, int SPEC = WALK_GENERIC>
 __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_start, int m_start, int n_steps,
                            uint64_t key, uint64_t stream, uint64_t base0, int p0, int p1, const NormalSrc &ns,
                            double *vals, int *s_next, double *path_out, int32_t *stop_out,
@@ -137,7 +140,13 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
       R agg;
       bool stop;
       R pay;
-      if constexpr (GEO && !FAST && D > 1) {
+      if constexpr (SPEC == WALK_MAXCALL_CMC && D > 1) {
+        // payoff_agg's max-call branch and rule_stop's CMC branch
+        agg = aggregate<D>(M, v);
+        pay = r_sub(agg, M.strike);
+        pay = pay > (R)0 ? pay : (R)0;
+        stop = pay > (R)0 && (m == M.n_dates || cmc_stop<D>(M, m, v, agg));
+      } else if constexpr (SPEC == WALK_GEO && !FAST && D > 1) {
         R lv[D > 1 ? D : 1];
         pay = geo_payoff<D>(M, v, agg, lv);
         stop = pay > (R)0 && (m == M.n_dates || (M.rule == RULE_IZ ? iz_stop<D>(M, m, v, lv)
