@@ -90,7 +90,7 @@ struct SampleParams {
 struct KernelTriple {
   void *walk, *iz, *dec;
   void *iz_geo = nullptr;   // parity I&Z probes specialised for the geometric put (d > 1)
-  void *walk_mc = nullptr;  // walker specialised for the max-call payoff under a CMC rule (d > 1)
+  void *walk_cmc = nullptr;  // walker specialised for CMC rules (d > 1)
 };
 
 // Kernel families for launch accounting (brm_prof.cu, BRM_PROF_* in the C ABI).

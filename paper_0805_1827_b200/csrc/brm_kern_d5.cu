@@ -5,8 +5,8 @@ namespace brm {
 KernelTriple kernels_d5(bool fast) {
   if (fast)
     return KernelTriple{(void *)&walk_units<5, true>, (void *)&iz_probes<5, true>, (void *)&decisions<5, true>,
-                        nullptr, (void *)&walk_units<5, true, WALK_MAXCALL_CMC>};
+                        nullptr, (void *)&walk_units<5, true, WALK_CMC>};
   return KernelTriple{(void *)&walk_units<5, false>, (void *)&iz_probes<5, false>, (void *)&decisions<5, false>,
-                      (void *)&iz_probes<5, false, true>, (void *)&walk_units<5, false, WALK_MAXCALL_CMC>};
+                      (void *)&iz_probes<5, false, true>, (void *)&walk_units<5, false, WALK_CMC>};
 }
 }  // namespace brm

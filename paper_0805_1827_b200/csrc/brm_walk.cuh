@@ -93,9 +93,9 @@ __device__ __forceinline__ double geo_payoff(const Model<double> &M, const doubl
 
 // Specialised steps (each instance launched only for its payoff / rule; code
 // a kernel never runs still costs registers and instruction cache):
-// WALK_GEO: the geometric put (geo_payoff); WALK_MAXCALL_CMC: the max-call
-// payoff under a CMC rule.
-enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_MAXCALL_CMC = 2 };
+// WALK_GEO: the geometric put (geo_payoff); WALK_CMC: a CMC rule (the
+// labels and pricing of C3-C5).
+enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_CMC = 2 };
 
 template <int D, bool FAST, int SPEC = WALK_GENERIC>
 __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_start, int m_start, int n_steps,
@@ -140,11 +140,9 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
       R agg;
       bool stop;
       R pay;
-      if constexpr (SPEC == WALK_MAXCALL_CMC && D > 1) {
-        // payoff_agg's max-call branch and rule_stop's CMC branch
-        agg = aggregate<D>(M, v);
-        pay = r_sub(agg, M.strike);
-        pay = pay > (R)0 ? pay : (R)0;
+      if constexpr (SPEC == WALK_CMC && D > 1) {
+        // rule_stop's CMC branch only (no I&Z surface code in the kernel)
+        pay = payoff_agg<D>(M, v, agg);
         stop = pay > (R)0 && (m == M.n_dates || cmc_stop<D>(M, m, v, agg));
       } else if constexpr (SPEC == WALK_GEO && !FAST && D > 1) {
         R lv[D > 1 ? D : 1];
