@@ -53,12 +53,12 @@ CONFIGS = {
 
 # fp64-pipe lane-operations per executed asset-step of the parity walker,
 # measured by ncu on the C5 label launch (DADD+DMUL+DFMA+DSETP thread
-# instructions / executed asset-steps; profiles/r01b_walk_c5_sass_mix.txt):
+# instructions / executed asset-steps; profiles/r01c_walk_c5_sass_mix.txt):
 # AS241 central ~33 + divide ~9 + exp ~17 + uniform/step ~6 + rule compares.
-DP_OPS_PER_ASSET_STEP = 80.4
+DP_OPS_PER_ASSET_STEP = 80.7
 # DRAM bytes per walker launch from the same capture (dram__bytes_read+write,
-# profiles/r01b_walk_c5_labels_pricing.txt): label launch 983.6 KB, pricing 103.7 KB
-WALK_DRAM_BYTES_PER_LAUNCH = (983.6e3 + 103.7e3) / 2
+# profiles/r01c_walk_c5_labels_pricing.txt): label launch 981.0 KB, pricing 100.9 KB
+WALK_DRAM_BYTES_PER_LAUNCH = (981.0e3 + 100.9e3) / 2
 FP64_LANES_PER_SM = 64
 N_SMS = 148
 
@@ -284,7 +284,7 @@ def run_engine(args, cfg):
                          "peak": peak if mode == "parity" else None, "unit": "TFLOP/s",
                          "frac": achieved / peak if achieved is not None else None,
                          "asset_steps_per_s": kern_steps * cfg["d"] / (kern_ms / 1e3) if kern_ms > 0 else None,
-                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r01b capture)",
+                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r01c capture)",
                          "kernel": "walk_units+iz_probes",
                          "work": f"{DP_OPS_PER_ASSET_STEP:g} fp64 lane-ops (ncu-measured) x executed asset-steps "
                                  f"({kern_steps // max(args.steps, 1)} path-steps x d per step)",
