@@ -9,7 +9,7 @@
 //     s_k = s_{k-1} + R_E(w_k) * ulp_E,  R_E(w) = round-to-nearest(w / ulp_E)
 // as long as w / ulp_E is not an exact tie (whose rounding depends on the
 // parity of s_{k-1}) and the sum stays below 2^(E+1).  So a warp converts a
-// tile of 32 x kChainT weights to integers R_E(w) = rint(w / ulp_E) and
+// tile of 32 x T weights to integers R_E(w) = rint(w / ulp_E) and
 // prefix-sums them -- in fp64, where every integer below 2^53 and every
 // power-of-two scaling is exact, so the sums are exact and associative --
 // and writes s_k = M_k * ulp_E.  The first element that leaves the binade, is a
@@ -33,11 +33,6 @@ __device__ long long g_chain_stats[6];  // tiles, events, seq elements, seq cycl
 #else
 #define BRM_CHAIN_STAT(i, v)
 #endif
-
-// Positive normal s = M * 2^(E - 1075), M in [2^52, 2^53) <-> bits (E - 1) << 52 | ... + M.
-__device__ __forceinline__ double chain_value(int E, long long M) {
-  return __longlong_as_double(((long long)(E - 1) << 52) + M);
-}
 
 // Storage position of chain element j: padded arrays insert one slot after
 // every 16 elements, so the 16-element runs of consecutive lanes start in
