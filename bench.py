@@ -61,6 +61,12 @@ DP_OPS_PER_ASSET_STEP = 80.7
 WALK_DRAM_BYTES_PER_LAUNCH = (981.0e3 + 100.9e3) / 2
 FP64_LANES_PER_SM = 64
 N_SMS = 148
+# fast mode (fp32 Box-Muller) walker: issue-bound (ncu issue slots 68%, ALU
+# 46%, XU 23% on the C5 label launch).  Thread instructions per executed
+# asset-step of the d = 10 walker, ncu-measured (profiles/r01c_walk_c5_fast.txt);
+# peak = 4 schedulers x 32 lanes per SM per clock.
+FAST_INST_PER_ASSET_STEP_D10 = 76.2
+ISSUE_LANES_PER_SM = 128
 
 
 def sigma_of(cfg):
@@ -251,10 +257,12 @@ def run_engine(args, cfg):
     sm_mhz = clocks["sm_mhz"] or 1965.0
     peak = FP64_LANES_PER_SM * N_SMS * sm_mhz * 1e6 / 1e12  # T fp64 lane-ops/s at the sampled clock
     if mode == "fast":
-        peak *= 2.0  # fp32 lanes
+        peak = ISSUE_LANES_PER_SM * N_SMS * sm_mhz * 1e6 / 1e12  # T thread-instructions/s issue peak
     if mode == "parity":
         achieved = (kern_steps * cfg["d"] * DP_OPS_PER_ASSET_STEP) / (kern_ms / 1e3) / 1e12 if kern_ms > 0 else 0.0
-    else:  # fast mode: no calibrated op model yet; report the rate, no fraction
+    elif cfg["d"] == 10 and kern_ms > 0:  # fast mode: the instruction model is calibrated on d = 10
+        achieved = (kern_steps * cfg["d"] * FAST_INST_PER_ASSET_STEP_D10) / (kern_ms / 1e3) / 1e12
+    else:
         achieved = None
     total_launches = sum(v[1] for v in prof.values())
     total_kernel_ms = sum(v[0] for v in prof.values())
@@ -280,17 +288,20 @@ def run_engine(args, cfg):
                     "note": "public API (numpy in/out) wall clock incl. host staging"},
             "gpu_launches": total_launches // max(args.steps, 1),
             "kernel_ms_per_step": {k: v[0] / max(args.steps, 1) for k, v in prof.items() if v[1]},
-            "roofline": {"bound": "fp64-pipe" if mode == "parity" else "fp32/sfu-issue", "achieved": achieved,
-                         "peak": peak if mode == "parity" else None, "unit": "TFLOP/s",
+            "roofline": {"bound": "fp64-pipe" if mode == "parity" else "issue", "achieved": achieved,
+                         "peak": peak if achieved is not None else None,
+                         "unit": "TFLOP/s" if mode == "parity" else "T thread-instructions/s",
                          "frac": achieved / peak if achieved is not None else None,
                          "asset_steps_per_s": kern_steps * cfg["d"] / (kern_ms / 1e3) if kern_ms > 0 else None,
                          "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r01c capture)",
                          "kernel": "walk_units+iz_probes",
-                         "work": f"{DP_OPS_PER_ASSET_STEP:g} fp64 lane-ops (ncu-measured) x executed asset-steps "
+                         "work": (f"{DP_OPS_PER_ASSET_STEP:g} fp64 lane-ops" if mode == "parity" else
+                                  f"{FAST_INST_PER_ASSET_STEP_D10:g} thread-instructions") + " (ncu-measured) x executed asset-steps "
                                  f"({kern_steps // max(args.steps, 1)} path-steps x d per step)",
                          "kernel_ms_per_step": kern_ms / max(args.steps, 1),
                          "launches_per_step": kern_launches / max(args.steps, 1),
-                         "peak_source": "nominal 148 SM x 64 fp64 lanes x sampled SM clock"},
+                         "peak_source": "nominal 148 SM x " + ("64 fp64 lanes" if mode == "parity" else
+                                                                "4 schedulers x 32 lanes") + " x sampled SM clock"},
             "clocks": clocks,
         }
         if world == 1 and not args.no_cpu_baseline:
