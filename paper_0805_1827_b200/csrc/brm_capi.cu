@@ -299,7 +299,10 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   const int smem = P.vals_offset + 8 * P.chunk;
   if (smem > c->info.max_smem) return fail(BRM_EINVAL, "model image too large for shared memory (%d B)", smem);
   BRM_TRY(call.scratch<double>(2 * (size_t)P.n_items, &P.partials));
-  void *kwalk = (c->hdr.rule == BRM_RULE_CMC && c->kern.walk_cmc && !P.normals) ? c->kern.walk_cmc : c->kern.walk;
+  // the CMC instance assumes even draw indices at every step for even d (parity mode)
+  const bool even_ok = c->fast() || c->hdr.d % 2 == 1 || (P.draw_base % 2 == 0);
+  void *kwalk = (c->hdr.rule == BRM_RULE_CMC && c->kern.walk_cmc && !P.normals && even_ok) ? c->kern.walk_cmc
+                                                                                            : c->kern.walk;
   BRM_TRY(allow_smem(kwalk, smem));
   int per_sm = 0;
   BRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kwalk, kWalkThreads, smem));

@@ -37,7 +37,7 @@ using RealT = typename std::conditional<FAST, float, double>::type;
 
 // Draws of step k of a path: parity indices base + k*d + a (reference
 // _core.pyx:4-7); fast positions pos + k*dp + a.
-template <int D, bool FAST>
+template <int D, bool FAST, bool EVEN = false>
 __device__ __forceinline__ void path_step_draws(int d, const PhiloxKey &K, uint64_t base, int k,
                                                 const NormalSrc &ns, RealT<FAST> *z, bool active,
                                                 const TailQueue &tq) {
@@ -50,7 +50,7 @@ __device__ __forceinline__ void path_step_draws(int d, const PhiloxKey &K, uint6
   if constexpr (FAST) {
     step_draws_fast<D>(K, base + (uint64_t)k * (uint64_t)fast_dp(d), z, d);
   } else if constexpr (D > 0) {
-    step_draws_compact<D>(K, base + (uint64_t)k * (uint64_t)d, z, active, tq.buf, tq.idx);
+    step_draws_compact<D, EVEN>(K, base + (uint64_t)k * (uint64_t)d, z, active, tq.buf, tq.idx);
   } else {
     step_draws<D>(K, base + (uint64_t)k * (uint64_t)d, z, d);
   }
@@ -127,7 +127,8 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
     // lanes without a path draw at a valid dummy index and discard the result
     constexpr bool kFused = FAST && D > 0;
     const bool fused = kFused && !ns.ptr && M.chol_lower != 0;  // full (non-triangular) factor: generic step
-    if (!fused) path_step_draws<D, FAST>(d, K, base, k, ns, z, have, tq);
+    // the CMC instance is launched only with even draw bases (host check)
+    if (!fused) path_step_draws<D, FAST, SPEC == WALK_CMC && D % 2 == 0>(d, K, base, k, ns, z, have, tq);
     if (have) {
       ++nsteps;
       if constexpr (kFused) {
