@@ -301,8 +301,11 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   BRM_TRY(call.scratch<double>(2 * (size_t)P.n_items, &P.partials));
   // the CMC instance assumes even draw indices at every step for even d (parity mode)
   const bool even_ok = c->fast() || c->hdr.d % 2 == 1 || (P.draw_base % 2 == 0);
-  void *kwalk = (c->hdr.rule == BRM_RULE_CMC && c->kern.walk_cmc && !P.normals && even_ok) ? c->kern.walk_cmc
-                                                                                            : c->kern.walk;
+  void *kwalk = c->kern.walk;
+  if (c->hdr.rule == BRM_RULE_CMC && !P.normals && even_ok) {
+    if (c->hdr.unit_diag && c->kern.walk_cmc_unit) kwalk = c->kern.walk_cmc_unit;
+    else if (c->kern.walk_cmc) kwalk = c->kern.walk_cmc;
+  }
   BRM_TRY(allow_smem(kwalk, smem));
   int per_sm = 0;
   BRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kwalk, kWalkThreads, smem));

@@ -5,8 +5,10 @@ namespace brm {
 KernelTriple kernels_d10(bool fast) {
   if (fast)
     return KernelTriple{(void *)&walk_units<10, true>, (void *)&iz_probes<10, true>, (void *)&decisions<10, true>,
-                        nullptr, (void *)&walk_units<10, true, WALK_CMC>};
+                        nullptr, (void *)&walk_units<10, true, WALK_CMC>,
+                        (void *)&walk_units<10, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<10, false>, (void *)&iz_probes<10, false>, (void *)&decisions<10, false>,
-                      (void *)&iz_probes<10, false, true>, (void *)&walk_units<10, false, WALK_CMC>};
+                      (void *)&iz_probes<10, false, true>, (void *)&walk_units<10, false, WALK_CMC>,
+                      (void *)&walk_units<10, false, WALK_CMC_UNIT>};
 }
 }  // namespace brm

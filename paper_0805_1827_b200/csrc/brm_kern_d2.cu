@@ -5,8 +5,10 @@ namespace brm {
 KernelTriple kernels_d2(bool fast) {
   if (fast)
     return KernelTriple{(void *)&walk_units<2, true>, (void *)&iz_probes<2, true>, (void *)&decisions<2, true>,
-                        nullptr, (void *)&walk_units<2, true, WALK_CMC>};
+                        nullptr, (void *)&walk_units<2, true, WALK_CMC>,
+                        (void *)&walk_units<2, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<2, false>, (void *)&iz_probes<2, false>, (void *)&decisions<2, false>,
-                      (void *)&iz_probes<2, false, true>, (void *)&walk_units<2, false, WALK_CMC>};
+                      (void *)&iz_probes<2, false, true>, (void *)&walk_units<2, false, WALK_CMC>,
+                      (void *)&walk_units<2, false, WALK_CMC_UNIT>};
 }
 }  // namespace brm

@@ -5,8 +5,10 @@ namespace brm {
 KernelTriple kernels_d3(bool fast) {
   if (fast)
     return KernelTriple{(void *)&walk_units<3, true>, (void *)&iz_probes<3, true>, (void *)&decisions<3, true>,
-                        nullptr, (void *)&walk_units<3, true, WALK_CMC>};
+                        nullptr, (void *)&walk_units<3, true, WALK_CMC>,
+                        (void *)&walk_units<3, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<3, false>, (void *)&iz_probes<3, false>, (void *)&decisions<3, false>,
-                      (void *)&iz_probes<3, false, true>, (void *)&walk_units<3, false, WALK_CMC>};
+                      (void *)&iz_probes<3, false, true>, (void *)&walk_units<3, false, WALK_CMC>,
+                      (void *)&walk_units<3, false, WALK_CMC_UNIT>};
 }
 }  // namespace brm

@@ -5,8 +5,10 @@ namespace brm {
 KernelTriple kernels_d5(bool fast) {
   if (fast)
     return KernelTriple{(void *)&walk_units<5, true>, (void *)&iz_probes<5, true>, (void *)&decisions<5, true>,
-                        nullptr, (void *)&walk_units<5, true, WALK_CMC>};
+                        nullptr, (void *)&walk_units<5, true, WALK_CMC>,
+                        (void *)&walk_units<5, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<5, false>, (void *)&iz_probes<5, false>, (void *)&decisions<5, false>,
-                      (void *)&iz_probes<5, false, true>, (void *)&walk_units<5, false, WALK_CMC>};
+                      (void *)&iz_probes<5, false, true>, (void *)&walk_units<5, false, WALK_CMC>,
+                      (void *)&walk_units<5, false, WALK_CMC_UNIT>};
 }
 }  // namespace brm

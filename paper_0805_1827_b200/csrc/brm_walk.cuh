@@ -94,8 +94,9 @@ __device__ __forceinline__ double geo_payoff(const Model<double> &M, const doubl
 // Specialised steps (each instance launched only for its payoff / rule; code
 // a kernel never runs still costs registers and instruction cache):
 // WALK_GEO: the geometric put (geo_payoff); WALK_CMC: a CMC rule (the
-// labels and pricing of C3-C5).
-enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_CMC = 2 };
+// labels and pricing of C3-C5); WALK_CMC_UNIT: a CMC rule with independent
+// assets (unit diagonal factor: C3, C5).
+enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_CMC = 2, WALK_CMC_UNIT = 3 };
 
 template <int D, bool FAST, int SPEC = WALK_GENERIC>
 __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_start, int m_start, int n_steps,
@@ -127,11 +128,18 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
     // lanes without a path draw at a valid dummy index and discard the result
     constexpr bool kFused = FAST && D > 0;
     const bool fused = kFused && !ns.ptr && M.chol_lower != 0;  // full (non-triangular) factor: generic step
-    // the CMC instance is launched only with even draw bases (host check)
-    if (!fused) path_step_draws<D, FAST, SPEC == WALK_CMC && D % 2 == 0>(d, K, base, k, ns, z, have, tq);
+    // the CMC instances are launched only with even draw bases (host check)
+    constexpr bool kCmc = SPEC == WALK_CMC || SPEC == WALK_CMC_UNIT;
+    if (!fused) path_step_draws<D, FAST, kCmc && D % 2 == 0>(d, K, base, k, ns, z, have, tq);
     if (have) {
       ++nsteps;
-      if constexpr (kFused) {
+      if constexpr (SPEC == WALK_CMC_UNIT && FAST && D > 0) {
+        fast_step_diag<(D > 0 ? D : 1)>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
+      } else if constexpr (SPEC == WALK_CMC_UNIT && !FAST) {
+        // y_i = 0 + 1.0 * z_i == z_i exactly (gbm_step's unit-diagonal branch)
+#pragma unroll
+        for (int i = 0; i < dim_of<D>(d); ++i) v[i] = r_mul(v[i], r_exp(r_add(M.mu[i], r_mul(M.vol[i], z[i]))));
+      } else if constexpr (kFused) {
         if (!fused) gbm_step<D>(M, v, z);
         else fast_step_fused<(D > 0 ? D : 1)>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
       } else {
@@ -141,7 +149,7 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
       R agg;
       bool stop;
       R pay;
-      if constexpr (SPEC == WALK_CMC && D > 1) {
+      if constexpr (kCmc && D > 1) {
         // rule_stop's CMC branch only (no I&Z surface code in the kernel)
         pay = payoff_agg<D>(M, v, agg);
         stop = pay > (R)0 && (m == M.n_dates || cmc_stop<D>(M, m, v, agg));
