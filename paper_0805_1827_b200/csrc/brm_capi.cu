@@ -303,7 +303,7 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   const bool even_ok = c->fast() || c->hdr.d % 2 == 1 || (P.draw_base % 2 == 0);
   void *kwalk = c->kern.walk;
   if (c->hdr.rule == BRM_RULE_CMC && !P.normals && even_ok) {
-    if (c->hdr.unit_diag && c->kern.walk_cmc_unit) kwalk = c->kern.walk_cmc_unit;
+    if (c->hdr.unit_diag && c->hdr.payoff == BRM_PAY_MAXCALL && c->kern.walk_cmc_unit) kwalk = c->kern.walk_cmc_unit;
     else if (c->kern.walk_cmc) kwalk = c->kern.walk_cmc;
   }
   BRM_TRY(allow_smem(kwalk, smem));

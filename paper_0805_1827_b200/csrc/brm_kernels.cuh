@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(kWalkThreads, (FAST && D < 20) ? 3 : 2) walk_u
   const Model<R> M = load_model<R>(P.hdr, P.blob, smem);
   double *vals = reinterpret_cast<double *>(smem + P.vals_offset);
   const int d = M.d;
-  const NormalSrc ns{P.normals, P.nrm_base, P.nrm_count};
+  // the specialised instances never run on supplied normals (host check)
+  const NormalSrc ns = SPEC == WALK_GENERIC ? NormalSrc{P.normals, P.nrm_base, P.nrm_count} : NormalSrc{nullptr, 0, 0};
 
   for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
     const int u = item / P.chunks_per_unit;

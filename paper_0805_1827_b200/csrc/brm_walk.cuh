@@ -94,8 +94,8 @@ __device__ __forceinline__ double geo_payoff(const Model<double> &M, const doubl
 // Specialised steps (each instance launched only for its payoff / rule; code
 // a kernel never runs still costs registers and instruction cache):
 // WALK_GEO: the geometric put (geo_payoff); WALK_CMC: a CMC rule (the
-// labels and pricing of C3-C5); WALK_CMC_UNIT: a CMC rule with independent
-// assets (unit diagonal factor: C3, C5).
+// labels and pricing of C3-C5); WALK_CMC_UNIT: the max-call payoff under a
+// CMC rule with independent assets (unit diagonal factor: C3, C5).
 enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_CMC = 2, WALK_CMC_UNIT = 3 };
 
 template <int D, bool FAST, int SPEC = WALK_GENERIC>
@@ -149,7 +149,13 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
       R agg;
       bool stop;
       R pay;
-      if constexpr (kCmc && D > 1) {
+      if constexpr (SPEC == WALK_CMC_UNIT && D > 1) {
+        // max-call payoff (payoff_agg's branch) under the CMC rule
+        agg = aggregate<D>(M, v);
+        pay = r_sub(agg, M.strike);
+        pay = pay > (R)0 ? pay : (R)0;
+        stop = pay > (R)0 && (m == M.n_dates || cmc_stop<D>(M, m, v, agg));
+      } else if constexpr (kCmc && D > 1) {
         // rule_stop's CMC branch only (no I&Z surface code in the kernel)
         pay = payoff_agg<D>(M, v, agg);
         stop = pay > (R)0 && (m == M.n_dates || cmc_stop<D>(M, m, v, agg));
