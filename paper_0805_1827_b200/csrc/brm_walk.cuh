@@ -150,8 +150,16 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
       bool stop;
       R pay;
       if constexpr (SPEC == WALK_CMC_UNIT && D > 1) {
-        // max-call payoff (payoff_agg's branch) under the CMC rule
-        agg = aggregate<D>(M, v);
+        // max-call payoff under the CMC rule (aggregate's max: strict >, first
+        // maximum; written out for fp32, where it schedules better)
+        if constexpr (FAST) {
+          agg = v[0];
+#pragma unroll
+          for (int i = 1; i < D; ++i)
+            if (v[i] > agg) agg = v[i];
+        } else {
+          agg = aggregate<D>(M, v);
+        }
         pay = r_sub(agg, M.strike);
         pay = pay > (R)0 ? pay : (R)0;
         stop = pay > (R)0 && (m == M.n_dates || cmc_stop<D>(M, m, v, agg));
