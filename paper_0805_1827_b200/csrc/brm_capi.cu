@@ -304,6 +304,7 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   void *kwalk = c->kern.walk;
   if (c->hdr.rule == BRM_RULE_CMC && !P.normals && even_ok) {
     if (c->hdr.unit_diag && c->hdr.payoff == BRM_PAY_MAXCALL && c->kern.walk_cmc_unit) kwalk = c->kern.walk_cmc_unit;
+    else if (c->fast() && c->hdr.chol_lower == 1 && c->kern.walk_cmc_lower) kwalk = c->kern.walk_cmc_lower;
     else if (c->kern.walk_cmc) kwalk = c->kern.walk_cmc;
   }
   BRM_TRY(allow_smem(kwalk, smem));

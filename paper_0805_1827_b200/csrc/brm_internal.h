@@ -92,6 +92,7 @@ struct KernelTriple {
   void *iz_geo = nullptr;   // parity I&Z probes specialised for the geometric put (d > 1)
   void *walk_cmc = nullptr;       // walker specialised for CMC rules (d > 1)
   void *walk_cmc_unit = nullptr;  // ... max-call payoff, independent assets (unit diagonal factor)
+  void *walk_cmc_lower = nullptr; // ... fast mode, lower-triangular factor
 };
 
 // Kernel families for launch accounting (brm_prof.cu, BRM_PROF_* in the C ABI).

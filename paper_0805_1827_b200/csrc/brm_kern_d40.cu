@@ -5,7 +5,8 @@ namespace brm {
 KernelTriple kernels_d40(bool fast) {
   if (fast)
     return KernelTriple{(void *)&walk_units<40, true>, (void *)&iz_probes<40, true>, (void *)&decisions<40, true>,
-                        nullptr, (void *)&walk_units<40, true, WALK_CMC>};
+                        nullptr, (void *)&walk_units<40, true, WALK_CMC>, nullptr,
+                        (void *)&walk_units<40, true, WALK_CMC_LOWER>};
   return KernelTriple{(void *)&walk_units<40, false>, (void *)&iz_probes<40, false>, (void *)&decisions<40, false>,
                       nullptr, (void *)&walk_units<40, false, WALK_CMC>};
 }

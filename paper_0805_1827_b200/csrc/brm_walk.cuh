@@ -95,8 +95,9 @@ __device__ __forceinline__ double geo_payoff(const Model<double> &M, const doubl
 // a kernel never runs still costs registers and instruction cache):
 // WALK_GEO: the geometric put (geo_payoff); WALK_CMC: a CMC rule (the
 // labels and pricing of C3-C5); WALK_CMC_UNIT: the max-call payoff under a
-// CMC rule with independent assets (unit diagonal factor: C3, C5).
-enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_CMC = 2, WALK_CMC_UNIT = 3 };
+// CMC rule with independent assets (unit diagonal factor: C3, C5);
+// WALK_CMC_LOWER: fast mode, CMC rule, lower-triangular factor (C4).
+enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_CMC = 2, WALK_CMC_UNIT = 3, WALK_CMC_LOWER = 4 };
 
 template <int D, bool FAST, int SPEC = WALK_GENERIC>
 __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_start, int m_start, int n_steps,
@@ -129,11 +130,13 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
     constexpr bool kFused = FAST && D > 0;
     const bool fused = kFused && !ns.ptr && M.chol_lower != 0;  // full (non-triangular) factor: generic step
     // the CMC instances are launched only with even draw bases (host check)
-    constexpr bool kCmc = SPEC == WALK_CMC || SPEC == WALK_CMC_UNIT;
+    constexpr bool kCmc = SPEC == WALK_CMC || SPEC == WALK_CMC_UNIT || SPEC == WALK_CMC_LOWER;
     if (!fused) path_step_draws<D, FAST, kCmc && D % 2 == 0>(d, K, base, k, ns, z, have, tq);
     if (have) {
       ++nsteps;
-      if constexpr (SPEC == WALK_CMC_UNIT && FAST && D > 0) {
+      if constexpr (SPEC == WALK_CMC_LOWER && FAST && D > 0) {
+        fast_step_fused<(D > 0 ? D : 1), true>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
+      } else if constexpr (SPEC == WALK_CMC_UNIT && FAST && D > 0) {
         fast_step_diag<(D > 0 ? D : 1)>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
       } else if constexpr (SPEC == WALK_CMC_UNIT && !FAST) {
         // y_i = 0 + 1.0 * z_i == z_i exactly (gbm_step's unit-diagonal branch)
