@@ -53,19 +53,19 @@ CONFIGS = {
 
 # fp64-pipe lane-operations per executed asset-step of the parity walker,
 # measured by ncu on the C5 label launch (DADD+DMUL+DFMA+DSETP thread
-# instructions / executed asset-steps; profiles/r01c_walk_c5_sass_mix.txt):
+# instructions / executed asset-steps; profiles/r01d_walk_c5_sass_mix.txt):
 # AS241 central ~33 + divide ~9 + exp ~17 + uniform/step ~6 + rule compares.
 DP_OPS_PER_ASSET_STEP = 80.7
 # DRAM bytes per walker launch from the same capture (dram__bytes_read+write,
-# profiles/r01c_walk_c5_labels_pricing.txt): label launch 981.0 KB, pricing 100.9 KB
-WALK_DRAM_BYTES_PER_LAUNCH = (981.0e3 + 100.9e3) / 2
+# profiles/r01d_walk_c5_labels_pricing.txt): label launch 972.3 KB, pricing 92.4 KB
+WALK_DRAM_BYTES_PER_LAUNCH = (972.3e3 + 92.4e3) / 2
 FP64_LANES_PER_SM = 64
 N_SMS = 148
 # fast mode (fp32 Box-Muller) walker: issue-bound (ncu issue slots 68%, ALU
 # 46%, XU 23% on the C5 label launch).  Thread instructions per executed
-# asset-step of the d = 10 walker, ncu-measured (profiles/r01c_walk_c5_fast.txt);
+# asset-step of the d = 10 walker, ncu-measured (profiles/r01d_walk_c5_fast.txt);
 # peak = 4 schedulers x 32 lanes per SM per clock.
-FAST_INST_PER_ASSET_STEP_D10 = 76.2
+FAST_INST_PER_ASSET_STEP_D10 = 72.8
 ISSUE_LANES_PER_SM = 128
 
 
@@ -293,7 +293,7 @@ def run_engine(args, cfg):
                          "unit": "TFLOP/s" if mode == "parity" else "T thread-instructions/s",
                          "frac": achieved / peak if achieved is not None else None,
                          "asset_steps_per_s": kern_steps * cfg["d"] / (kern_ms / 1e3) if kern_ms > 0 else None,
-                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r01c capture)",
+                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r01d capture)",
                          "kernel": "walk_units+iz_probes",
                          "work": (f"{DP_OPS_PER_ASSET_STEP:g} fp64 lane-ops" if mode == "parity" else
                                   f"{FAST_INST_PER_ASSET_STEP_D10:g} thread-instructions") + " (ncu-measured) x executed asset-steps "
