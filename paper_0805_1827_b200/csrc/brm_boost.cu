@@ -27,6 +27,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <functional>
 #include <cmath>
 #include <string>
@@ -1295,19 +1296,29 @@ extern "C" int brm_lstsq(int32_t device, void *stream, const double *design, con
   cudaSetDevice(device);
   retain_pool(device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  double *d_design = nullptr, *d_levels = nullptr, *d_coeffs = nullptr;
-  int *d_cols = nullptr, *d_rank = nullptr;
+  // one device block: [coeffs nb][rank 1 (as int, in a double slot)][design n*nb][levels n][cols nb (int)],
+  // so the full-rank case costs one allocation, one result copy and one sync
+  unsigned char *blk = nullptr;
   std::vector<int> cols(nb);
+  double hres[kLsMaxB + 1];  // coeffs, then the rank (an int) in the next slot
   int rank = 0;
   for (int c = 0; c < nb; ++c) cols[c] = c;
   const size_t smem_full = sizeof(double) * ((size_t)nb * n + n);
-  BCU(cudaMallocAsync(&d_design, sizeof(double) * (size_t)n * nb, s));
+  const size_t off_rank = sizeof(double) * nb;
+  const size_t off_design = off_rank + sizeof(double);
+  const size_t off_levels = off_design + sizeof(double) * (size_t)n * nb;
+  const size_t off_cols = off_levels + sizeof(double) * n;
+  const size_t blk_bytes = off_cols + sizeof(int) * nb;
+  double *d_coeffs, *d_design, *d_levels;
+  int *d_rank, *d_cols;
+  BCU(cudaMallocAsync(&blk, blk_bytes, s));
+  d_coeffs = reinterpret_cast<double *>(blk);
+  d_rank = reinterpret_cast<int *>(blk + off_rank);
+  d_design = reinterpret_cast<double *>(blk + off_design);
+  d_levels = reinterpret_cast<double *>(blk + off_levels);
+  d_cols = reinterpret_cast<int *>(blk + off_cols);
   BCU(cudaMemcpyAsync(d_design, design, sizeof(double) * (size_t)n * nb, cudaMemcpyDefault, s));
-  BCU(cudaMallocAsync(&d_levels, sizeof(double) * n, s));
   BCU(cudaMemcpyAsync(d_levels, levels, sizeof(double) * n, cudaMemcpyDefault, s));
-  BCU(cudaMallocAsync(&d_coeffs, sizeof(double) * nb, s));
-  BCU(cudaMallocAsync(&d_cols, sizeof(int) * nb, s));
-  BCU(cudaMallocAsync(&d_rank, sizeof(int), s));
   BCU(cudaMemcpyAsync(d_cols, cols.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
   BCU(cudaFuncSetAttribute(lstsq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
   {
@@ -1316,8 +1327,9 @@ extern "C" int brm_lstsq(int32_t device, void *stream, const double *design, con
     prof_end(tok, s);
   }
   BCU(cudaGetLastError());
-  BCU(cudaMemcpyAsync(&rank, d_rank, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BCU(cudaMemcpyAsync(hres, blk, off_rank + sizeof(int), cudaMemcpyDeviceToHost, s));
   BCU(cudaStreamSynchronize(s));
+  std::memcpy(&rank, reinterpret_cast<unsigned char *>(hres) + off_rank, sizeof(int));
   *out_rank_deficient = rank < nb;
   if (rank < nb) {
     // keep [1, z_a, z_a^2], zero the cross terms (boundary_iz.py:264-275)
@@ -1334,13 +1346,15 @@ extern "C" int brm_lstsq(int32_t device, void *stream, const double *design, con
                                                                         (int)keep.size(), d_coeffs, d_rank);
     prof_end(tok, s);
     BCU(cudaGetLastError());
+    BCU(cudaMemcpyAsync(hres, blk, off_rank, cudaMemcpyDeviceToHost, s));
+    BCU(cudaStreamSynchronize(s));
   }
-  BCU(cudaMemcpyAsync(out_coeffs, d_coeffs, sizeof(double) * nb, cudaMemcpyDefault, s));
-  BCU(cudaStreamSynchronize(s));
+  std::memcpy(out_coeffs, hres, sizeof(double) * nb);
 done:
-  for (void *p : {(void *)d_design, (void *)d_levels, (void *)d_coeffs, (void *)d_cols, (void *)d_rank})
-    if (p) cudaFreeAsync(p, s);
-  cudaStreamSynchronize(s);
+  if (blk) {
+    cudaFreeAsync(blk, s);
+    if (rc != BRM_OK) cudaStreamSynchronize(s);
+  }
   if (prev >= 0) cudaSetDevice(prev);
   return rc;
 }
