@@ -169,6 +169,14 @@ int fetch(const T *src, size_t count, std::vector<T> &dst, const char *name) {
   dst.assign(count, T());
   if (count == 0) return BRM_OK;
   if (!src) return fail(BRM_EINVAL, "%s is NULL", name);
+  // host arrays (the usual case: numpy packs) are copied on the host; a
+  // cudaMemcpy per array is a driver round trip each
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, src) != cudaSuccess) cudaGetLastError();
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) {
+    std::memcpy(dst.data(), src, count * sizeof(T));
+    return BRM_OK;
+  }
   BRM_CUDA(cudaMemcpy(dst.data(), src, count * sizeof(T), cudaMemcpyDefault));
   return BRM_OK;
 }
