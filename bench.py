@@ -51,21 +51,27 @@ CONFIGS = {
                n_paths=1 << 24, sampler="bridge", mode="parity"),
 }
 
-# fp64-pipe lane-operations per executed asset-step of the parity walker,
-# measured by ncu on the C5 label launch (DADD+DMUL+DFMA+DSETP thread
-# instructions / executed asset-steps; profiles/r01d_walk_c5_sass_mix.txt):
-# AS241 central ~33 + divide ~9 + exp ~17 + uniform/step ~6 + rule compares.
-DP_OPS_PER_ASSET_STEP = 80.7
+# ALGORITHMIC fp64 operations per executed asset-step of the parity pipeline
+# (SURVEY.md section 8(d)): AS241 central ~33 DP + divide + the 15% tail share
+# (log + sqrt), 53-bit uniform 2, GBM step 3, exp 17 -> ~70 DP instructions.
+# This is the work the roofline counts, independent of this build's SASS.
+DP_OPS_PER_ASSET_STEP = 70.0
+# What the walker actually executes on the fp64 pipe (ncu: DADD+DMUL+DFMA+DSETP
+# thread instructions / executed asset-steps on the C5 label launch,
+# profiles/r01d_walk_c5_sass_mix.txt): reported beside it as overhead.
+DP_OPS_EXECUTED_NCU = 80.7
 # DRAM bytes per walker launch from the same capture (dram__bytes_read+write,
 # profiles/r01d_walk_c5_labels_pricing.txt): label launch 972.3 KB, pricing 92.4 KB
 WALK_DRAM_BYTES_PER_LAUNCH = (972.3e3 + 92.4e3) / 2
 FP64_LANES_PER_SM = 64
 N_SMS = 148
 # fast mode (fp32 Box-Muller) walker: issue-bound (ncu issue slots 68%, ALU
-# 46%, XU 23% on the C5 label launch).  Thread instructions per executed
-# asset-step of the d = 10 walker, ncu-measured (profiles/r01d_walk_c5_fast.txt);
-# peak = 4 schedulers x 32 lanes per SM per clock.
-FAST_INST_PER_ASSET_STEP_D10 = 72.8
+# 46%, XU 23% on the C5 label launch).  ALGORITHMIC thread instructions per
+# asset-step: 3 MUFU + ~8 FP32 + ~15 INT (Philox,
+# 1/4 call per normal) + ~5 other = 31; peak = 4 schedulers x 32 lanes per SM
+# per clock.  The d = 10 walker executes 72.8 (ncu, profiles/r01d_walk_c5_fast.txt).
+FAST_INST_PER_ASSET_STEP = 31.0
+FAST_INST_EXECUTED_NCU_D10 = 72.8
 ISSUE_LANES_PER_SM = 128
 
 
@@ -258,12 +264,9 @@ def run_engine(args, cfg):
     peak = FP64_LANES_PER_SM * N_SMS * sm_mhz * 1e6 / 1e12  # T fp64 lane-ops/s at the sampled clock
     if mode == "fast":
         peak = ISSUE_LANES_PER_SM * N_SMS * sm_mhz * 1e6 / 1e12  # T thread-instructions/s issue peak
-    if mode == "parity":
-        achieved = (kern_steps * cfg["d"] * DP_OPS_PER_ASSET_STEP) / (kern_ms / 1e3) / 1e12 if kern_ms > 0 else 0.0
-    elif cfg["d"] == 10 and kern_ms > 0:  # fast mode: the instruction model is calibrated on d = 10
-        achieved = (kern_steps * cfg["d"] * FAST_INST_PER_ASSET_STEP_D10) / (kern_ms / 1e3) / 1e12
-    else:
-        achieved = None
+    ops = DP_OPS_PER_ASSET_STEP if mode == "parity" else FAST_INST_PER_ASSET_STEP
+    executed = DP_OPS_EXECUTED_NCU if mode == "parity" else FAST_INST_EXECUTED_NCU_D10
+    achieved = (kern_steps * cfg["d"] * ops) / (kern_ms / 1e3) / 1e12 if kern_ms > 0 else None
     total_launches = sum(v[1] for v in prof.values())
     total_kernel_ms = sum(v[0] for v in prof.values())
 
@@ -286,8 +289,11 @@ def run_engine(args, cfg):
             "e2e": {"value": work / wall, "unit": "path-steps/s", "h2d_bytes_per_step": h2d // max(args.steps, 1),
                     "d2h_bytes_per_step": d2h // max(args.steps, 1),
                     "note": "public API (numpy in/out) wall clock incl. host staging"},
+            "value_basis": "CUDA events on the launch stream around the public-API call (host gaps included); "
+                           "kernel_ms_total_per_step is the sum of the library's own kernel times",
             "gpu_launches": total_launches // max(args.steps, 1),
             "kernel_ms_per_step": {k: v[0] / max(args.steps, 1) for k, v in prof.items() if v[1]},
+            "kernel_ms_total_per_step": total_kernel_ms / max(args.steps, 1),
             "roofline": {"bound": "fp64-pipe" if mode == "parity" else "issue", "achieved": achieved,
                          "peak": peak if achieved is not None else None,
                          "unit": "TFLOP/s" if mode == "parity" else "T thread-instructions/s",
@@ -295,17 +301,20 @@ def run_engine(args, cfg):
                          "asset_steps_per_s": kern_steps * cfg["d"] / (kern_ms / 1e3) if kern_ms > 0 else None,
                          "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r01d capture)",
                          "kernel": "walk_units+iz_probes",
-                         "work": (f"{DP_OPS_PER_ASSET_STEP:g} fp64 lane-ops" if mode == "parity" else
-                                  f"{FAST_INST_PER_ASSET_STEP_D10:g} thread-instructions") + " (ncu-measured) x executed asset-steps "
-                                 f"({kern_steps // max(args.steps, 1)} path-steps x d per step)",
+                         "work": (f"{ops:g} algorithmic " + ("fp64 ops" if mode == "parity" else "thread-instructions")
+                                  + " per asset-step (SURVEY.md 8(d)) x executed asset-steps "
+                                  f"({kern_steps // max(args.steps, 1)} path-steps x d per step)"),
+                         "executed_per_asset_step_ncu": executed,
+                         "pipe_utilisation": (achieved * executed / ops / peak) if achieved is not None else None,
                          "kernel_ms_per_step": kern_ms / max(args.steps, 1),
                          "launches_per_step": kern_launches / max(args.steps, 1),
-                         "peak_source": "nominal 148 SM x " + ("64 fp64 lanes" if mode == "parity" else
-                                                                "4 schedulers x 32 lanes") + " x sampled SM clock"},
+                         "peak_source": "of NOMINAL peak: 148 SM x " + ("64 fp64 lanes" if mode == "parity" else
+                                                                "4 schedulers x 32 lanes") + " x sampled SM clock "
+                                        "(MEASURED_PEAKS.json has no fp64 / issue figure)"},
             "clocks": clocks,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg)
+            line["cpu_baseline"] = cpu_baseline(cfg, full=args.cpu_baseline == "full")
         if alt is not None:
             line["fast_mode"] = alt
     if world > 1:
@@ -341,14 +350,14 @@ def reference_step(sample, B, engine):
     return B.price(params, spec, B.IzRule(b), sample["n_paths"], SEED, engine=engine), float(np.mean(rep.iteration_counts))
 
 
-def cpu_baseline(cfg, steps: int = 1) -> dict:
+def cpu_baseline(cfg, steps: int = 1, full: bool = True) -> dict:
     try:
         from oracle import reference as R
         from oracle.oracle import cpu_count
         B = R.bermuda()
     except ImportError as exc:
         return {"value": None, "unit": "path-steps/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {exc}"}
-    sample = reference_sample(cfg)
+    sample = dict(cfg) if full else reference_sample(cfg)
     cores = cpu_count()
     engine = B.Engine(workers=cores, pool="process")
     t = []
@@ -359,7 +368,8 @@ def cpu_baseline(cfg, steps: int = 1) -> dict:
         t.append(time.perf_counter() - t0)
     work = nominal_path_steps(sample, iters)
     return {"value": work / float(np.mean(t)), "unit": "path-steps/s", "cores": cores, "kind": "reference",
-            "sample": (f"{sample['name']} with n_train={sample.get('n_train')} n_paths={sample['n_paths']} "
+            "sample": ((f"the FULL {sample['name']} config, one run: " if full else f"{sample['name']} sample: ") +
+                       f"n_train={sample.get('n_train')} n_paths={sample['n_paths']} "
                        f"({work:.3g} nominal path-steps), unmodified reference (oracle/_ref, Cython walker, "
                        f"Engine(workers={cores}, pool='process')), {np.mean(t):.1f} s per run"),
             "seconds_per_run": float(np.mean(t))}
@@ -414,6 +424,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
     ap.add_argument("--mode", choices=("parity", "fast"), default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-baseline", choices=("full", "sample"), default="full",
+                    help="time the reference CPU pricer on the full config (default) or the bounded sample")
     ap.add_argument("--no-fast-line", action="store_true", help="skip the fast-mode companion measurement")
     ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
     ap.add_argument("--scale", type=float, default=1.0, help="scale n_train / n_paths (tests only)")

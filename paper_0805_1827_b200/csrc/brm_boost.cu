@@ -1289,6 +1289,11 @@ extern "C" int brm_lstsq(int32_t device, void *stream, const double *design, con
   if (nb < 1 || nb > kLsMaxB) return bfail(BRM_EINVAL, "basis size out of range");
   if (n64 < nb) return bfail(BRM_EINVAL, "need at least " + std::to_string(nb) + " probe points for the quadratic fit, got " + std::to_string(n64));
   if (n64 > kLsMaxN) return bfail(BRM_EINVAL, "too many probe points for the device fit");
+  // the rank-deficient fallback keeps columns [1, z_a, z_a^2] of the quadratic basis
+  // (packs.py:74-93), so the design must be that basis of k coordinates
+  if (k < 0 || nb != 1 + k + k * (k + 1) / 2)
+    return bfail(BRM_EINVAL, "basis size " + std::to_string(nb) + " is not the quadratic basis of " +
+                                 std::to_string(k) + " coordinates");
   const int n = (int)n64;
   int rc = BRM_OK;
   int prev = -1;
@@ -1349,7 +1354,11 @@ extern "C" int brm_lstsq(int32_t device, void *stream, const double *design, con
     BCU(cudaMemcpyAsync(hres, blk, off_rank, cudaMemcpyDeviceToHost, s));
     BCU(cudaStreamSynchronize(s));
   }
-  std::memcpy(out_coeffs, hres, sizeof(double) * nb);
+  if (is_dev(out_coeffs)) {
+    BCU(cudaMemcpyAsync(out_coeffs, d_coeffs, sizeof(double) * nb, cudaMemcpyDeviceToDevice, s));
+  } else {
+    std::memcpy(out_coeffs, hres, sizeof(double) * nb);
+  }
 done:
   if (blk) {
     cudaFreeAsync(blk, s);

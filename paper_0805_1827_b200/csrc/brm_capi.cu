@@ -231,6 +231,7 @@ struct brm_ctx {
   KernelTriple kern{};
   double *normals = nullptr;  // supplied-normals copy (device)
   cudaEvent_t ready = nullptr;  // image upload complete (waited on by every launch stream)
+  cudaEvent_t retired = nullptr;  // scratch event: work of a stream the context stops using
   uint64_t nrm_base = 0, nrm_count = 0;
   int capacity = 0;  // > 0: slotted CMC image (brm_ctx_create_cmc)
   SlotDims slot{};
@@ -672,14 +673,38 @@ int brm_ctx_set_ensemble(brm_ctx *c, int32_t date, const int32_t *feat, const do
   return call.finish();
 }
 
+namespace {
+// Order the context's own stream after everything already enqueued on the
+// stream it launched on last, so frees on the own stream never overtake a
+// launch that reads the image.  A caller stream that no longer exists cannot
+// take the event record: then wait for the whole device instead.
+void retire_user_stream(brm_ctx *c) {
+  if (!c->has_user_stream || c->user_stream == c->own_stream) return;
+  if (!c->retired && cudaEventCreateWithFlags(&c->retired, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+    return;
+  }
+  if (cudaEventRecord(c->retired, c->user_stream) != cudaSuccess ||
+      cudaStreamWaitEvent(c->own_stream, c->retired, 0) != cudaSuccess) {
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+  }
+}
+}  // namespace
+
 int brm_ctx_destroy(brm_ctx *c) {
   if (!c) return BRM_OK;
   DeviceScope scope(c->device);
-  // freed in stream order after every launch that used the image
-  const cudaStream_t s = c->stream();
+  // freed in stream order on the context's own (per-device, library-owned)
+  // stream, after every launch that used the image on it or on the caller's
+  // last stream
+  retire_user_stream(c);
+  const cudaStream_t s = c->own_stream;
   if (c->blob) cudaFreeAsync(c->blob, s);
   if (c->normals) cudaFreeAsync(c->normals, s);
   if (c->ready) cudaEventDestroy(c->ready);
+  if (c->retired) cudaEventDestroy(c->retired);
   cudaGetLastError();
   delete c;
   return BRM_OK;
@@ -687,6 +712,18 @@ int brm_ctx_destroy(brm_ctx *c) {
 
 int brm_ctx_set_stream(brm_ctx *c, void *s) {
   if (!c) return fail(BRM_EINVAL, "NULL context");
+  DeviceScope scope(c->device);
+  const cudaStream_t next = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+  if (next != c->stream()) {
+    // work already enqueued on the previous stream is ordered before later
+    // launches on the new one, and before the image is freed
+    if (c->has_user_stream) retire_user_stream(c);
+    if (next != c->own_stream) {
+      if (!c->retired) BRM_CUDA(cudaEventCreateWithFlags(&c->retired, cudaEventDisableTiming));
+      BRM_CUDA(cudaEventRecord(c->retired, c->own_stream));
+      BRM_CUDA(cudaStreamWaitEvent(next, c->retired, 0));
+    }
+  }
   c->user_stream = static_cast<cudaStream_t>(s);
   c->has_user_stream = s != nullptr;
   return BRM_OK;
@@ -1105,7 +1142,9 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   int csize = 8;
   while (csize > 1 && (int64_t)csize * kWalkThreads / 2 > n_inner) csize >>= 1;
   while (csize > 1 && n * csize > 2LL * c->info.sms) csize >>= 1;
-  const int per_cta = (n_inner + csize - 1) / csize;
+  const int per_cta = iz_per_cta(n_inner, csize);
+  if (per_cta > kIzMaxChunks * kIzFoldChunk)
+    return fail(BRM_EINVAL, "%d inner paths per probe CTA exceed %d", per_cta, kIzMaxChunks * kIzFoldChunk);
   P.vals_offset = smem_model(c);
   P.steps = step_counter(PK_IZ);
   P.hist_offset = P.vals_offset + ((8 * per_cta + 15) & ~15);

@@ -13,6 +13,15 @@ constexpr int kWalkThreads = 256;   // threads per walker CTA
 constexpr int kPathBlock = 4096;    // pricer.py:32 PATH_BLOCK (stream convention)
 constexpr int kPriceChunk = 1024;   // paths per pricing work item (4 per block)
 constexpr int kMaxChunk = 2048;     // largest chunk a walker CTA folds in smem
+constexpr int kIzFoldChunk = 256;   // I&Z probes: paths per fixed-order fold chunk
+constexpr int kIzMaxChunks = 64;    // fold chunks per probe CTA (16384 inner paths)
+
+// Inner paths per CTA of an I&Z probe cluster: whole fold chunks, so the
+// chunk boundaries (and the summation order) do not depend on the cluster size.
+__host__ __device__ inline int iz_per_cta(int n_inner, int csize) {
+  const int per = (n_inner + csize - 1) / csize;
+  return (per + kIzFoldChunk - 1) / kIzFoldChunk * kIzFoldChunk;
+}
 
 struct WalkParams {
   ModelHdr hdr;

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
   __shared__ int s_next;
   __shared__ R s_start[kMaxD];
   __shared__ double s_state[kMaxD];
-  __shared__ double s_part;                 // this CTA's partial sum
+  __shared__ double s_chunk[kIzMaxChunks];  // this CTA's 256-path chunk sums
   __shared__ double s_x, s_lo, s_hi;        // rank 0: solver state
   __shared__ int s_done, s_it, s_armed, s_conv;
   const Model<R> M = load_model<R>(P.hdr, P.blob, smem);
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
   }
   const double *seedp = P.seeds + (size_t)probe * P.seed_stride;
   const int asset = P.assets ? P.assets[probe] : 0;
-  const int per_cta = (P.n_inner + csize - 1) / csize;
+  const int per_cta = iz_per_cta(P.n_inner, csize);
   const int p0 = rank * per_cta;
   const int p1 = min(p0 + per_cta, P.n_inner);
   const uint64_t per_path = (uint64_t)P.n_steps * (uint64_t)d;
@@ -178,13 +178,23 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
                                                           vals, &s_next, nullptr,
                           nullptr, P.steps, tq);
     __syncthreads();
-    double s = 0.0, q = 0.0;
-    fold_values(vals, p1 > p0 ? p1 - p0 : 0, s_red, s, q);
-    if (threadIdx.x == 0) s_part = s;
+    // fixed-order fold in 256-path chunks: the chunk sums are added in path
+    // order by rank 0, so the continuation value does not depend on the
+    // cluster size (i.e. on how many probes share the GPU)
+    for (int c = 0; p0 + c * kIzFoldChunk < p1; ++c) {
+      double s = 0.0, q = 0.0;
+      fold_values(vals + c * kIzFoldChunk, min(kIzFoldChunk, p1 - p0 - c * kIzFoldChunk), s_red, s, q);
+      if (threadIdx.x == 0) s_chunk[c] = s;
+      __syncthreads();
+    }
     cluster.sync();
     if (rank == 0 && threadIdx.x == 0) {
       double total = 0.0;
-      for (int r = 0; r < csize; ++r) total = __dadd_rn(total, *cluster.map_shared_rank(&s_part, r));
+      for (int r = 0; r < csize; ++r) {
+        const double *rc = cluster.map_shared_rank(s_chunk, r);
+        for (int c = 0; r * per_cta + c * kIzFoldChunk < min((r + 1) * per_cta, P.n_inner); ++c)
+          total = __dadd_rn(total, rc[c]);
+      }
       const double cont = __ddiv_rn(total, (double)P.n_inner);
       const int n_it = it + 1;
       s_it = n_it;
