@@ -210,12 +210,16 @@ def _build_device_loop(params, spec, cfg, seed, sampler, mode, shard, torch, str
     for m in range(nd - 1, 0, -1):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
-        lo, hi = shard.range(cfg.n_train)
-        feats = torch.empty((hi - lo, F), dtype=f64, device="cuda")
-        betas = torch.empty((hi - lo,), dtype=f64, device="cuda")
-        if hi > lo:
-            _be.cmc_calc(mp, None, m, seed, lo, hi - lo, cfg.n_label, bridge_scalars(params, spec, m), sampler,
-                         feats, betas, mode=mode, ctx=ctx)
+        ranges = shard.local_ranges(cfg.n_train)
+        rows = sum(hi - lo for lo, hi in ranges)
+        feats = torch.empty((rows, F), dtype=f64, device="cuda")
+        betas = torch.empty((rows,), dtype=f64, device="cuda")
+        off = 0
+        for lo, hi in ranges:
+            if hi > lo:
+                _be.cmc_calc(mp, None, m, seed, lo, hi - lo, cfg.n_label, bridge_scalars(params, spec, m), sampler,
+                             feats[off:off + hi - lo], betas[off:off + hi - lo], mode=mode, ctx=ctx)
+            off += hi - lo
         feats = shard.all_gather_rows(feats, cfg.n_train)
         betas = shard.all_gather_rows(betas, cfg.n_train)
         ev[1].record(stream)
@@ -277,15 +281,20 @@ def build_cmc_rule(params, spec, cfg: CmcBuildConfig, seed: int = 0, engine=None
         later = rule.pack()
         bridge = bridge_scalars(params, spec, m)
         t0 = time.perf_counter()
-        lo, hi = shard.range(cfg.n_train)
+        ranges = shard.local_ranges(cfg.n_train)
         if torch is not None:
             # device-resident date step: features and labels stay in HBM, every
             # launch (sampler, walker, AdaBoost) is ordered on torch's stream
             get_context(mp, later, mode=mode).set_stream(stream)
-            feats = torch.empty((hi - lo, F), dtype=torch.float64, device="cuda")
-            betas = torch.empty((hi - lo,), dtype=torch.float64, device="cuda")
-            if hi > lo:
-                _be.cmc_calc(mp, later, m, seed, lo, hi - lo, cfg.n_label, bridge, sampler, feats, betas, mode=mode)
+            rows = sum(hi - lo for lo, hi in ranges)
+            feats = torch.empty((rows, F), dtype=torch.float64, device="cuda")
+            betas = torch.empty((rows,), dtype=torch.float64, device="cuda")
+            off = 0
+            for lo, hi in ranges:
+                if hi > lo:
+                    _be.cmc_calc(mp, later, m, seed, lo, hi - lo, cfg.n_label, bridge, sampler,
+                                 feats[off:off + hi - lo], betas[off:off + hi - lo], mode=mode)
+                off += hi - lo
             feats = shard.all_gather_rows(feats, cfg.n_train)
             betas = shard.all_gather_rows(betas, cfg.n_train)
         else:

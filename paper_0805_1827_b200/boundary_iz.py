@@ -241,13 +241,13 @@ def build_iz_boundary(params, spec, j_points: int, n_inner: int, epsilon: float 
     for m in range(spec.n_dates - 1, 0, -1):
         later = boundary.pack()
         t0 = time.perf_counter()
-        lo, hi = shard.range(n_items)
         res = np.zeros((n_items, 3))
-        if hi > lo:
-            lv, it, cv = _be.iz_solve_batch(mp, later, item_seed[lo:hi], item_asset[lo:hi], m, n_inner,
-                                            solver=solver, epsilon=epsilon, max_iter=max_iter, avg_window=5,
-                                            lo=lo_b, hi=hi_b, tol=tol, seed=seed, item_lo=lo, mode=mode)
-            res[lo:hi] = np.stack([lv, it, cv], axis=1)
+        for lo, hi in shard.local_ranges(n_items):
+            if hi > lo:
+                lv, it, cv = _be.iz_solve_batch(mp, later, item_seed[lo:hi], item_asset[lo:hi], m, n_inner,
+                                                solver=solver, epsilon=epsilon, max_iter=max_iter, avg_window=5,
+                                                lo=lo_b, hi=hi_b, tol=tol, seed=seed, item_lo=lo, mode=mode)
+                res[lo:hi] = np.stack([lv, it, cv], axis=1)
         if shard.distributed:
             import torch
             t = torch.from_numpy(res).cuda()

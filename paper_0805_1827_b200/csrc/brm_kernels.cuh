@@ -103,6 +103,24 @@ __device__ inline double probe_state(const ModelHdr &h, const double *seed, int 
   return x;
 }
 
+// Fixed-order sums of vals[0..n) in chunks of kIzFoldChunk paths into
+// s_chunk[]: warp w folds chunks w, w + 8, ...; lane l adds the chunk's
+// values l, l + 32, ... in order, then a fixed shuffle tree.  One barrier.
+__device__ __forceinline__ void fold_chunks(const double *vals, int n, double *s_chunk) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nck = (n + kIzFoldChunk - 1) / kIzFoldChunk;
+  for (int c = warp; c < nck; c += blockDim.x >> 5) {
+    const double *v = vals + c * kIzFoldChunk;
+    const int len = min(kIzFoldChunk, n - c * kIzFoldChunk);
+    double s = 0.0;
+    for (int j = lane; j < len; j += 32) s = __dadd_rn(s, v[j]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
+    if (lane == 0) s_chunk[c] = s;
+  }
+  __syncthreads();
+}
+
 // GEOK: the geometric-put instance (walk_paths' GEO step; launched only for
 // that payoff).
 template <int D, bool FAST, bool GEOK = false>
@@ -181,12 +199,7 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
     // fixed-order fold in 256-path chunks: the chunk sums are added in path
     // order by rank 0, so the continuation value does not depend on the
     // cluster size (i.e. on how many probes share the GPU)
-    for (int c = 0; p0 + c * kIzFoldChunk < p1; ++c) {
-      double s = 0.0, q = 0.0;
-      fold_values(vals + c * kIzFoldChunk, min(kIzFoldChunk, p1 - p0 - c * kIzFoldChunk), s_red, s, q);
-      if (threadIdx.x == 0) s_chunk[c] = s;
-      __syncthreads();
-    }
+    fold_chunks(vals, p1 > p0 ? p1 - p0 : 0, s_chunk);
     cluster.sync();
     if (rank == 0 && threadIdx.x == 0) {
       double total = 0.0;

@@ -16,15 +16,23 @@ The fits (AdaBoost, least squares) are deterministic device kernels, so
 every rank runs them on the gathered data and gets the same rule; no
 broadcast is needed.  With world size 1 every collective is a no-op and
 torch.distributed is never touched.
+
+``virtual_shards(n)`` runs the same decomposition inside one process: every
+phase is executed range by range for all n partitions (the reference's task
+partition, engine.py:65-81, with nb_tasks = n) and nothing is exchanged.  It
+is how the reference CLI's determinism bench (cli.py:281-319) checks that a
+price does not depend on the partition, on a box with one GPU.
 """
 
 from __future__ import annotations
 
+import contextlib
+import threading
 from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["Shard", "current", "partition_ranges"]
+__all__ = ["Shard", "current", "partition_ranges", "virtual_shards"]
 
 
 def partition_ranges(total: int, parts: int) -> list[tuple[int, int]]:
@@ -45,13 +53,22 @@ class Shard:
     rank: int = 0
     world: int = 1
     group: object = None
+    virtual: bool = False  # all partitions run in this process, one after another
 
     @property
     def distributed(self) -> bool:
-        return self.world > 1
+        """True when ranks are processes that exchange data through collectives."""
+        return self.world > 1 and not self.virtual
 
     def range(self, total: int) -> tuple[int, int]:
         return partition_ranges(total, self.world)[self.rank]
+
+    def local_ranges(self, total: int) -> list[tuple[int, int]]:
+        """The item ranges this process computes, in item order: its own rank's
+        range, or every partition's range under ``virtual_shards``."""
+        if self.virtual:
+            return partition_ranges(total, self.world)
+        return [self.range(total)]
 
     def all_gather_rows(self, local, total: int):
         """Concatenate each rank's contiguous rows (torch tensors on this rank's GPU)."""
@@ -80,8 +97,27 @@ class Shard:
             dist.barrier(group=self.group)
 
 
+_local = threading.local()
+
+
+@contextlib.contextmanager
+def virtual_shards(world: int):
+    """Run every phase as ``world`` contiguous partitions in this process."""
+    if world < 1:
+        raise ValueError(f"need at least one partition, got {world}")
+    prev = getattr(_local, "shard", None)
+    _local.shard = Shard(0, int(world), None, virtual=True)
+    try:
+        yield _local.shard
+    finally:
+        _local.shard = prev
+
+
 def current() -> Shard:
     """The shard of this process (torch.distributed world if initialised)."""
+    v = getattr(_local, "shard", None)
+    if v is not None:
+        return v
     try:
         import torch.distributed as dist
         if dist.is_available() and dist.is_initialized():

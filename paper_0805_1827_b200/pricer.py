@@ -103,8 +103,14 @@ def block_stats(mp, rp, n_paths: int, seed: int, mode=None, shard=None):
     """Per-block stats of every block, gathered across the job's GPUs -> numpy [n_blocks, 3]."""
     shard = shard or _current_shard()
     n_blocks = (n_paths + PATH_BLOCK - 1) // PATH_BLOCK
-    if not shard.distributed:
+    if shard.world == 1:
         return _be.price_blocks(mp, rp, n_paths, seed, 0, n_blocks, mode=mode)
+    if shard.virtual:  # every partition in this process, block ranges in order
+        table = np.empty((n_blocks, 3))
+        for lo, hi in shard.local_ranges(n_blocks):
+            if hi > lo:
+                _be.price_blocks(mp, rp, n_paths, seed, lo, hi, out=table[lo:hi], mode=mode)
+        return table
     import torch
     lo, hi = shard.range(n_blocks)
     table = torch.zeros((n_blocks, 3), dtype=torch.float64, device="cuda")
