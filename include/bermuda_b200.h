@@ -41,7 +41,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define BRM_ABI_VERSION 2
+#define BRM_ABI_VERSION 3
 
 enum brm_status {
     BRM_OK = 0,
@@ -135,9 +135,9 @@ int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t star
 /* Self-test of the walker's branch-free fp64 exp / divide / log / sqrt against
  * CUDA's exp / __ddiv_rn / log / __dsqrt_rn (kind 0 exp_nb(a), 1 exp(a),
  * 2 div_nb(a, b), 3 a / b, 4 log_nb(a), 5 log(a), 6 sqrt_nb(a), 7 sqrt(a)),
- * and of AdaBoost's warp-parallel cumsum against the sequential one (kind 8:
- * out = np.cumsum order of a[0..n) by one thread, 9: by the warp's binade
- * tiles; a >= 0). */
+ * and of AdaBoost's parallel cumsum against the sequential one (kind 8:
+ * out = np.cumsum order of a[0..n) by one thread, 10: by the parity
+ * AdaBoost's block-parallel exact scan; a >= 0). */
 int brm_selftest_math(int32_t device, int32_t kind, const double *a, const double *b, int64_t n, double *out);
 
 /* ---- Path walker ------------------------------------------------------- */
@@ -212,13 +212,19 @@ int brm_cmc_calc(brm_ctx *ctx, int32_t sampler, int32_t m, uint64_t seed, int64_
  * flags BRM_FIT_DEVICE_RESULT: every output (count and intercept included)
  * is a device pointer, the stump arrays are written in full ([rounds],
  * entries past *out_count unspecified) and the call returns without
- * synchronising: results are ordered on `stream`. */
+ * synchronising: results are ordered on `stream`.  out_n_pos (may be NULL;
+ * host or device) receives the number of positive labels, the report's
+ * positive_fraction * n (boundary_cmc.py:275).
+ * Parity mode runs the split search's cumsums as a block-parallel exact
+ * scan (integer adds inside a binade, one fp64 add per binade crossing), one
+ * CTA per feature and one grid barrier per round; the column sort is an own
+ * bitonic + merge-path kernel. */
 #define BRM_FIT_SINGLE_STUMP 1
 #define BRM_FIT_DEVICE_RESULT 2
 int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, void *stream, const double *xs,
                      const double *betas, const double *weights, int64_t n, int32_t F, int32_t rounds,
                      int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha, double *out_err,
-                     int32_t *out_count, double *out_intercept);
+                     int32_t *out_count, double *out_intercept, int32_t *out_n_pos);
 
 /* ---- Quadratic boundary regression (boundary_iz.py:250-276) ------------- */
 /* Least squares over the design [n*nb] (row-major), fp64 Householder QR with

@@ -20,7 +20,7 @@ BRM_OK, BRM_EINVAL, BRM_ENOMEM, BRM_ECUDA, BRM_ENODEV = range(5)
 MODE_PARITY, MODE_FAST = 0, 1
 FIT_SINGLE_STUMP = 1
 FIT_DEVICE_RESULT = 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -79,7 +79,7 @@ _SIGNATURES = {
                                C.c_void_p, C.c_void_p, C.c_void_p]),
     "brm_fit_ensemble": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
-                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "brm_profile_enable": (C.c_int, [C.c_int32]),
     "brm_profile_reset": (C.c_int, []),
     "brm_profile_read": (C.c_int, [C.c_int32, _dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

@@ -201,7 +201,7 @@ def fit_ensemble_arrays(xs, betas, rounds: int, mode=None, device=None, weights=
     N.check(N.lib.brm_fit_ensemble(_dev(device), resolve_mode(mode), N.FIT_SINGLE_STUMP if single else 0,
                                    N.stream_handle(stream), N.ptr(xs), N.ptr(betas), N.ptr(w), n, F, r,
                                    N.ptr(feat), N.ptr(thr), N.ptr(pol), N.ptr(alpha), N.ptr(err),
-                                   C.addressof(count), C.addressof(icept)))
+                                   C.addressof(count), C.addressof(icept), None))
     c = count.value
     return feat[:c], thr[:c], pol[:c], alpha[:c], err[:c], float(icept.value)
 
@@ -209,13 +209,14 @@ def fit_ensemble_arrays(xs, betas, rounds: int, mode=None, device=None, weights=
 def fit_ensemble_device(xs, betas, rounds: int, out, mode=None, device=None, stream=None) -> None:
     """Device AdaBoost with device-resident results and no host synchronisation
     (BRM_FIT_DEVICE_RESULT): ``out`` holds device tensors feat[int32, rounds],
-    thr/pol/alpha/err[f64, rounds], count[int32, 1], intercept[f64, 1]."""
+    thr/pol/alpha/err[f64, rounds], count[int32, 1], intercept[f64, 1] and
+    optionally n_pos[int32, 1] (positive labels)."""
     from .context import resolve_mode
     n, F = int(xs.shape[0]), int(xs.shape[1])
     N.check(N.lib.brm_fit_ensemble(_dev(device), resolve_mode(mode), N.FIT_DEVICE_RESULT, N.stream_handle(stream),
                                    N.ptr(xs), N.ptr(betas), None, n, F, int(rounds), N.ptr(out["feat"]),
                                    N.ptr(out["thr"]), N.ptr(out["pol"]), N.ptr(out["alpha"]), N.ptr(out["err"]),
-                                   N.ptr(out["count"]), N.ptr(out["intercept"])))
+                                   N.ptr(out["count"]), N.ptr(out["intercept"]), N.ptr(out.get("n_pos"))))
 
 
 def lstsq(design, levels, k_coords: int, device=None, stream=None):

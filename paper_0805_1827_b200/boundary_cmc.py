@@ -205,7 +205,7 @@ def _build_device_loop(params, spec, cfg, seed, sampler, mode, shard, torch, str
            "err": torch.zeros((nd + 1, R), dtype=f64, device="cuda"),
            "count": torch.zeros((nd + 1,), dtype=i32, device="cuda"),
            "intercept": torch.full((nd + 1,), -1.0, dtype=f64, device="cuda")}
-    pos = torch.zeros((nd + 1,), dtype=f64, device="cuda")
+    n_pos = torch.zeros((nd + 1,), dtype=i32, device="cuda")
     marks = []
     for m in range(nd - 1, 0, -1):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -224,14 +224,15 @@ def _build_device_loop(params, spec, cfg, seed, sampler, mode, shard, torch, str
         betas = shard.all_gather_rows(betas, cfg.n_train)
         ev[1].record(stream)
         date_out = {k: (v[m] if v.dim() == 2 else v[m:m + 1]) for k, v in out.items()}
+        date_out["n_pos"] = n_pos[m:m + 1]
         _be.fit_ensemble_device(feats, betas, R, date_out, mode=mode, stream=stream)
         ctx.set_ensemble(m, date_out["feat"], date_out["thr"], date_out["pol"], date_out["alpha"],
                          date_out["count"], date_out["intercept"])
         ev[2].record(stream)
-        pos[m] = (betas > 0).to(f64).mean()
         marks.append((m, ev))
     host = {k: v.cpu().numpy() for k, v in out.items()}  # the build's one synchronisation
-    pos_h = pos.cpu().numpy()
+    # np.mean(betas > 0.0) (boundary_cmc.py:275): count / n in fp64
+    pos_h = n_pos.cpu().numpy().astype(np.float64) / cfg.n_train
     ensembles, report = {}, CmcBuildReport()
     for m, ev in marks:
         c = int(host["count"][m])

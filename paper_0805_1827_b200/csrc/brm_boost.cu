@@ -20,8 +20,6 @@
 
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_segmented_radix_sort.cuh>
 
 #include <algorithm>
 #include <climits>
@@ -35,7 +33,6 @@
 
 #include "../../include/bermuda_b200.h"
 #include "brm_internal.h"
-#include "brm_chain.cuh"
 #include "brm_rng.cuh"
 
 namespace cg = cooperative_groups;
@@ -43,7 +40,6 @@ namespace cg = cooperative_groups;
 namespace brm {
 
 constexpr int kBoostThreads = 256;
-constexpr int kTile = 4096;
 constexpr int kPwBlock = 128;  // numpy PW_BLOCKSIZE
 
 // numpy pairwise_sum leaf (n <= 128): 8 strided accumulators, fixed combine,
@@ -150,38 +146,6 @@ static int pw_tree(int64_t n, PwTree &t) {
   return newid[root];
 }
 
-struct BoostParams {
-  int n, F, rounds;
-  const double *xs;        // [n][F]
-  const double *xsorted;   // [F][n]
-  const double *xt;        // [F][n] columns in sample order
-  const double *y;         // [n] +-1
-  double *w;               // [n] unnormalised weights of the current round
-  double *wn;              // [F][n] per-CTA normalised copy (w / sum(w), numpy order)
-  const int *pos_idx;      // [F][n] sample ids of the positives in sorted order (first n_pos[f])
-  const int *neg_idx;      // [F][n] sample ids of the negatives in sorted order
-  const int *cntpos;       // [F][n] positives among sorted positions 0..i
-  const int2 *brk;         // [F][n] chain indices at split i (INT_MIN: no break after i)
-  double *pcum, *ncum;     // [F][n] prefix sums of the positive / negative chains
-  const int2 *leaves;
-  int n_leaves;
-  const int2 *children;
-  const int *level_end;
-  int n_levels, root;
-  int tree_smem;           // 1: copy the tree tables into shared memory
-  double *feat_err;        // [F]
-  int *feat_pos;           // [F] 2*i + (pol == -1)
-  double *wsub;            // [F][n] per-CTA scratch for the constant-stump sums
-  double *leafsum;         // [L] pairwise leaf sums of w (written by the reweighting CTAs)
-  int *out_feat;
-  double *out_thr, *out_pol, *out_alpha, *out_err;
-  int *out_count;
-  double *out_intercept;
-  const int *n_pos;        // positives in the training set (device)
-  int raw;  // 1: one fit_stump search with the given weights, no boosting rules
-  long long *timing;  // optional per-phase clock64 totals of CTA 0 (diagnostics)
-};
-
 // The recursion tree as the kernel reads it (shared-memory copy when it fits).
 struct PwView {
   const int2 *leaves, *children;
@@ -277,27 +241,6 @@ __device__ double cta_pairwise(const PwView &T, const double *a, double *s_node)
   return pw_tree_sum(T, s_node);
 }
 
-// s[j] = w[idx[j]] for j < cnt (cnt <= kTile): all index loads of a thread
-// are issued before the dependent value loads.
-__device__ __forceinline__ void gather_tile(const double *__restrict__ w, const int *__restrict__ idx, int cnt,
-                                            double *__restrict__ s) {
-  constexpr int G = kTile / kBoostThreads;
-  int id[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const int j = threadIdx.x + g * kBoostThreads;
-    id[g] = j < cnt ? __ldg(idx + j) : -1;
-  }
-  double v[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) v[g] = id[g] >= 0 ? w[id[g]] : 0.0;
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const int j = threadIdx.x + g * kBoostThreads;
-    if (j < cnt) s[chain_pos<true>(j)] = v[g];  // warp_chain's padded layout
-  }
-}
-
 // One class (boosting.py:185-187): a zero-round ensemble carrying the class
 // sign; decided on the device so a fit needs no host round trip.
 __device__ __forceinline__ bool one_class_exit(int raw, int n, int n_pos, int *out_count, double *out_intercept) {
@@ -324,318 +267,26 @@ __device__ __forceinline__ bool cand_less(const Cand &a, const Cand &b) {
   return a.err < b.err || (a.err == b.err && a.key < b.key);
 }
 
-// Chain self-test (brm_selftest_math kinds 8 / 9): the prefix sums of a[0..n)
-// by the one-thread sequential chain and by the warp's binade tiles.
+// Self-test reference (brm_selftest_math kind 8): np.cumsum of a[0..n) by one
+// thread, the sequential chain the exact scan (kind 10) must reproduce.
 __global__ void chain_selftest(int kind, const double *a, int64_t n, double *out) {
-  double acc = 0.0;
-  if (kind == 8) {
-    if (threadIdx.x == 0) serial_chain<false>(a, out, 0, (int)n, acc);
-  } else {
-    warp_chain<false>(a, out, (int)n, acc);
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) out[i] = acc = __dadd_rn(acc, a[i]);
   }
 }
 
 void *chain_selftest_kernel() { return (void *)&chain_selftest; }
 
-__global__ void __launch_bounds__(kBoostThreads) boost_kernel(BoostParams P) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double *s_node = reinterpret_cast<double *>(smem_raw);               // [L + I]
-  double *s_in_p = s_node + 2 * P.n_leaves;
-  constexpr int kTileP = chain_padded_len(kTile);  // padded tiles (chain_pos)
-  double *s_in_n = s_in_p + kTileP;
-  double *s_out_p = s_in_n + kTileP;
-  double *s_out_n = s_out_p + kTileP;
-  unsigned char *s_after = reinterpret_cast<unsigned char *>(s_out_n + kTileP);
-  __shared__ Cand s_cand[kBoostThreads / 32];
-  __shared__ int s_stop;
-  __shared__ double s_alpha, s_thr, s_pol, s_err;
-  __shared__ int s_feat;
+}  // namespace brm
+#include "brm_boost_exact.cuh"
+namespace brm {
 
-  const int n = P.n, F = P.F;
-  const int f = blockIdx.x;
-  const int n_pos_all = *P.n_pos;
-  if (one_class_exit(P.raw, n, n_pos_all, P.out_count, P.out_intercept)) return;
-  // reweighting slices are whole pairwise leaves, so each CTA also publishes
-  // the leaf sums of the new weights and sum(w) needs only the tree combine
-  const int L = P.n_leaves;
-  PwView T{P.leaves, P.children, P.level_end, L, P.n_levels, P.root};
-  if (P.tree_smem) {  // tree tables after the tiles: leaves, children, level ends
-    int2 *s_leaves = reinterpret_cast<int2 *>(s_after);
-    int2 *s_children = s_leaves + L;
-    int *s_level = reinterpret_cast<int *>(s_children + max(L - 1, 0));
-    for (int i = threadIdx.x; i < L; i += blockDim.x) s_leaves[i] = P.leaves[i];
-    for (int i = threadIdx.x; i < L - 1; i += blockDim.x) s_children[i] = P.children[i];
-    for (int i = threadIdx.x; i < P.n_levels; i += blockDim.x) s_level[i] = P.level_end[i];
-    T.leaves = s_leaves;
-    T.children = s_children;
-    T.level_end = s_level;
-    __syncthreads();
-  }
-  const int l_lo = (int)((long long)blockIdx.x * L / gridDim.x), l_hi = (int)((long long)(blockIdx.x + 1) * L / gridDim.x);
-  double *wn = P.wn + (size_t)f * n;
-  int count = 0;
-  // per-phase clock totals (diagnostics, BRM_BOOST_TIMING): thread 0 of CTA 0,
-  // slot 7 the positive-chain thread; kept in registers, stored at the end
-  const bool timed = P.timing && blockIdx.x == 0;
-  long long t_mark = 0, tacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-#define BRM_TSLOT(k)                       \
-  if (timed && threadIdx.x == 0) {         \
-    const long long now_ = clock64();      \
-    tacc[k] += now_ - t_mark;              \
-    t_mark = now_;                         \
-  }
+void *exact_scan_selftest_kernel() { return (void *)&exact_scan_selftest; }
 
-  for (int round = 0; round < P.rounds; ++round) {
-    if (timed && threadIdx.x == 0) t_mark = clock64();
-    // ---- wn = w / w.sum() (numpy pairwise order), CTA-private copy, and
-    // total = wn.sum() in the same pass ----------------------------------
-    double total;
-    if (round == 0) {
-      pw_leaf_sums(T, P.w, 0, L, s_node, PwIdentity{}, [&](int i, double v) { wn[i] = v; });
-      total = pw_tree_sum(T, s_node);
-    } else {
-      for (int l = threadIdx.x; l < L; l += blockDim.x) s_node[l] = __ldcg(P.leafsum + l);
-      const double s = pw_tree_sum(T, s_node);
-      if (timed && threadIdx.x == 0) tacc[9] += clock64() - t_mark;
-      pw_leaf_sums(
-          T, P.w, 0, L, s_node, [&](int, double x) { return div_nb(x, s); }, [&](int i, double v) { wn[i] = v; });
-      if (timed && threadIdx.x == 0) tacc[10] += clock64() - t_mark;
-      total = pw_tree_sum(T, s_node);
-    }
-    BRM_TSLOT(1);
-    // ---- split search on feature f -------------------------------------
-    if (f < F) {
-      const int *pid = P.pos_idx + (size_t)f * n;
-      const int *nid = P.neg_idx + (size_t)f * n;
-      double *pc = P.pcum + (size_t)f * n;
-      double *nc = P.ncum + (size_t)f * n;
-      const int n_pos = n_pos_all, n_neg = n - n_pos_all;
-      double pacc = 0.0, nacc = 0.0;  // np.cumsum(where(y>0, w, 0)): zeros never change a partial sum
-      // tiles: all threads gather, the two highest warps run the two sequential
-      // chains (the issue arbiter favours high warp ids), all threads write back
-      const int wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-      for (int t0 = 0; t0 < max(n_pos, n_neg); t0 += kTile) {
-        const int tp = max(0, min(kTile, n_pos - t0)), tn = max(0, min(kTile, n_neg - t0));
-        gather_tile(wn, pid + t0, tp, s_in_p);
-        gather_tile(wn, nid + t0, tn, s_in_n);
-        __syncthreads();
-        // one warp per chain: binade tiles (brm_chain.cuh), ~2x the sequential
-        // fp64 add chain's 9 cycles per element
-        if (wid == nwarp - 2) {
-          const long long c0 = timed ? clock64() : 0;
-          warp_chain<true, 32>(s_in_p, s_out_p, tp, pacc);
-          if (timed) tacc[7] += clock64() - c0;
-        } else if (wid == nwarp - 1) {
-          warp_chain<true, 32>(s_in_n, s_out_n, tn, nacc);
-        }
-        __syncthreads();
-        for (int j = threadIdx.x; j < tp; j += blockDim.x) pc[t0 + j] = s_out_p[chain_pos<true>(j)];
-        for (int j = threadIdx.x; j < tn; j += blockDim.x) nc[t0 + j] = s_out_n[chain_pos<true>(j)];
-      }
-      __syncthreads();
-    BRM_TSLOT(2);
-      // split points: brk[i] = (positives up to i) - 1, (negatives up to i) - 1,
-      // precomputed once per fit; x == INT_MIN marks "no distinct-value break"
-      const int2 *brk = P.brk + (size_t)f * n;
-      const double tot_neg = n_neg > 0 ? nc[n_neg - 1] : 0.0;
-      Cand best{__longlong_as_double(0x7ff0000000000000LL), 0x7fffffff};
-      constexpr int U = 16;
-      for (int i0 = threadIdx.x; i0 < n - 1; i0 += U * blockDim.x) {
-        int2 bi[U];
-        double pcs[U], ncs[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * blockDim.x;
-          bi[u] = i < n - 1 ? brk[i] : make_int2(INT_MIN, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          pcs[u] = bi[u].x >= 0 ? pc[bi[u].x] : 0.0;
-          ncs[u] = bi[u].y >= 0 ? nc[bi[u].y] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (bi[u].x == INT_MIN) continue;
-          const int i = i0 + u * blockDim.x;
-          const double ep = __dadd_rn(pcs[u], __dsub_rn(tot_neg, ncs[u]));
-          const double em = __dsub_rn(total, ep);
-          const Cand ca{ep, 2 * i}, cb{em, 2 * i + 1};
-          if (cand_less(ca, best)) best = ca;
-          if (cand_less(cb, best)) best = cb;
-        }
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        Cand o;
-        o.err = __shfl_down_sync(0xffffffffu, best.err, off);
-        o.key = __shfl_down_sync(0xffffffffu, best.key, off);
-        if (cand_less(o, best)) best = o;
-      }
-      if ((threadIdx.x & 31) == 0) s_cand[threadIdx.x >> 5] = best;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        for (int wi = 1; wi < (int)blockDim.x / 32; ++wi)
-          if (cand_less(s_cand[wi], best)) best = s_cand[wi];
-        P.feat_err[f] = best.err;
-        P.feat_pos[f] = best.key;
-      }
-    }
-    BRM_TSLOT(3);
-    grid.sync();
-    BRM_TSLOT(4);
-    // ---- pick the winner (every CTA, same answer) ------------------------
-    // first minimum over features in order: (err, feature) lexicographic
-    double be = __longlong_as_double(0x7ff0000000000000LL);
-    int bf = 0x7fffffff, bk = 0;
-    if (threadIdx.x < 32) {
-      for (int g = threadIdx.x; g < F; g += 32) {
-        const int pos = __ldcg(P.feat_pos + g);
-        const double e = __ldcg(P.feat_err + g);
-        if (pos != 0x7fffffff && e < be) {
-          be = e;
-          bf = g;
-          bk = pos;
-        }
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double oe = __shfl_down_sync(0xffffffffu, be, off);
-        const int of = __shfl_down_sync(0xffffffffu, bf, off);
-        const int ok = __shfl_down_sync(0xffffffffu, bk, off);
-        if (oe < be || (oe == be && of < bf)) {
-          be = oe;
-          bf = of;
-          bk = ok;
-        }
-      }
-    }
-    if (threadIdx.x == 0) {
-      if (bf == 0x7fffffff) bf = -1;
-      if (bf < 0) {
-        s_stop = 2;  // every feature constant: resolved below by the whole CTA
-        s_feat = 0;
-        s_thr = __longlong_as_double(0xfff0000000000000LL);
-      } else {
-        const int i = bk >> 1;
-        const double *xf = P.xsorted + (size_t)bf * n;
-        s_feat = bf;
-        s_thr = __dmul_rn(0.5, __dadd_rn(xf[i], xf[i + 1]));
-        s_pol = (bk & 1) ? -1.0 : 1.0;
-        s_err = be;
-        s_stop = 0;
-      }
-    }
-    __syncthreads();
-    if (s_stop == 2) {
-      // every feature constant (boosting.py:166-170): pol = +1 iff sum(w*y) >= 0,
-      // err = sum(w[y != pol]), both in numpy's pairwise order
-      double *ws = P.wsub + (size_t)blockIdx.x * n;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) ws[i] = __dmul_rn(wn[i], P.y[i]);
-      __syncthreads();
-      const double swy = cta_pairwise(T, ws, s_node);
-      const double pol = swy >= 0.0 ? 1.0 : -1.0;
-      if (threadIdx.x == 0) {
-        int k = 0;
-        for (int i = 0; i < n; ++i)
-          if (P.y[i] != pol) ws[k++] = wn[i];
-        s_pol = pol;
-        s_err = pw_serial(ws, k);
-        s_stop = 0;
-      }
-      __syncthreads();
-    }
-    // alpha = 0.5 * log((1 - err) / max(err, 1e-10)); stop rules of fit_ensemble
-    if (threadIdx.x == 0) {
-      const double err = s_err;
-      if (P.raw) {
-        if (blockIdx.x == 0) {
-          P.out_feat[0] = s_feat;
-          P.out_thr[0] = s_thr;
-          P.out_pol[0] = s_pol;
-          P.out_alpha[0] = 1.0;
-          P.out_err[0] = err;
-        }
-        s_stop = 3;
-      } else if (err >= 0.5) {
-        s_stop = 1;
-      } else {
-        const double a = __dmul_rn(0.5, log(__ddiv_rn(__dsub_rn(1.0, err), err > 1e-10 ? err : 1e-10)));
-        s_alpha = a;
-        if (blockIdx.x == 0) {
-          P.out_feat[count] = s_feat;
-          P.out_thr[count] = s_thr;
-          P.out_pol[count] = s_pol;
-          P.out_alpha[count] = a;
-          P.out_err[count] = err;
-        }
-        s_stop = err <= 0.0 ? 3 : 0;
-      }
-    }
-    __syncthreads();
-    if (s_stop == 1) break;
-    ++count;
-    if (s_stop == 3 || round + 1 == P.rounds) break;
-    BRM_TSLOT(5);
-    // ---- reweight own slice: w = (w / sum) * exp(-alpha * y * pred) ------
-    {
-      const double a = s_alpha, thr = s_thr, pol = s_pol;
-      const int feat = s_feat;
-      const double e_agree = exp(-a), e_miss = exp(a);
-      if (timed && threadIdx.x == 0) tacc[8] += clock64() - t_mark;
-      pw_leaf_sums(
-          T, wn, l_lo, l_hi, P.leafsum,
-          [&](int i, double x) {
-            const double pred = __ldg(P.xt + (size_t)feat * n + i) > thr ? pol : -pol;
-            return __dmul_rn(x, (__ldg(P.y + i) * pred > 0.0) ? e_agree : e_miss);
-          },
-          [&](int i, double v) { P.w[i] = v; });
-    }
-    if (timed && threadIdx.x == 0) tacc[0] += clock64() - t_mark;
-    grid.sync();
-    BRM_TSLOT(6);
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) write_result(count, n, n_pos_all, P.out_count, P.out_intercept);
-  if (timed && threadIdx.x == 0)
-    for (int k = 0; k < 12; ++k)
-      if (k != 7) P.timing[k] = tacc[k];
-  if (timed && threadIdx.x == blockDim.x - 64) P.timing[7] = tacc[7];
-#undef BRM_TSLOT
-}
-
-// Per feature: ids of positives / negatives in sorted order and the running
-// count of positives (once per fit; labels and order are fixed across rounds).
-__global__ void __launch_bounds__(256) split_classes(const int *order, const double *y, const double *xsorted, int n,
-                                                     int *pos_idx, int *neg_idx, int *cntpos, int2 *brk) {
-  using Scan = cub::BlockScan<int, 256>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int s_carry;
-  const int f = blockIdx.x;
-  const int *ord = order + (size_t)f * n;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (int t0 = 0; t0 < n; t0 += 256) {
-    const int i = t0 + threadIdx.x;
-    const int id = i < n ? ord[i] : 0;
-    const int pos = (i < n && y[id] > 0.0) ? 1 : 0;
-    int excl, tile_total;
-    Scan(tmp).ExclusiveSum(pos, excl, tile_total);
-    const int carry = s_carry;
-    if (i < n) {
-      const int before = carry + excl;  // positives strictly before position i
-      cntpos[(size_t)f * n + i] = before + pos;
-      if (pos) pos_idx[(size_t)f * n + before] = id;
-      else neg_idx[(size_t)f * n + (i - before)] = id;
-      const double *xf = xsorted + (size_t)f * n;
-      const bool is_break = i + 1 < n && __dsub_rn(xf[i + 1], xf[i]) > 0.0;  // boosting.py:145
-      const int np_ = before + pos, nn_ = i + 1 - np_;
-      brk[(size_t)f * n + i] = is_break ? make_int2(np_ - 1, nn_ - 1) : make_int2(INT_MIN, 0);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_carry = carry + tile_total;
-    __syncthreads();
-  }
-}
+}  // namespace brm
+#include "brm_boost_cluster.cuh"
+namespace brm {
 
 // ---------------------------------------------------------- fast mode ----
 // BRM_MODE_FAST AdaBoost: the same stump search and boosting rules, with the
@@ -1032,16 +683,19 @@ struct Scratch {
 extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, void *stream, const double *xs,
                                 const double *betas, const double *weights, int64_t n64, int32_t F, int32_t rounds,
                                 int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha,
-                                double *out_err, int32_t *out_count, double *out_intercept) {
+                                double *out_err, int32_t *out_count, double *out_intercept, int32_t *out_n_pos) {
   const bool raw = flags & BRM_FIT_SINGLE_STUMP;
   const bool dev_out = flags & BRM_FIT_DEVICE_RESULT;
   if (!xs || !betas || !out_count || !out_intercept) return bfail(BRM_EINVAL, "NULL argument");
   if (dev_out && !(is_dev(out_feat) && is_dev(out_thr) && is_dev(out_pol) && is_dev(out_alpha) && is_dev(out_err) &&
-                   is_dev(out_count) && is_dev(out_intercept)))
+                   is_dev(out_count) && is_dev(out_intercept) && (!out_n_pos || is_dev(out_n_pos))))
     return bfail(BRM_EINVAL, "BRM_FIT_DEVICE_RESULT needs device output pointers");
   if (rounds < 1) return bfail(BRM_EINVAL, "need at least one round, got " + std::to_string(rounds));
-  if (n64 < 1 || n64 > (1 << 26)) return bfail(BRM_EINVAL, "training set size out of range");
+  if (n64 < 1 || n64 > (int64_t)kCodeId) return bfail(BRM_EINVAL, "training set size out of range");
   if (F < 1 || F > 148) return bfail(BRM_EINVAL, "feature count out of range");
+  // every per-feature array is indexed [f * n + i] in 64-bit, but the kernels
+  // take n as int and the fast kernel's scans are int: keep n * F in int range
+  if (n64 * F > (int64_t)INT_MAX) return bfail(BRM_EINVAL, "training set too large (n * F > 2^31 - 1)");
   if (!out_feat || !out_thr || !out_pol || !out_alpha || !out_err) return bfail(BRM_EINVAL, "NULL stump outputs");
   const int n = (int)n64;
   if (raw) rounds = 1;
@@ -1053,12 +707,9 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   {
     Scratch S(s);
-    double *d_xs, *d_b, *d_xt, *d_xsorted, *d_y, *d_w, *d_wn, *d_pc, *d_nc, *d_err, *d_wsub, *d_thr, *d_pol,
-        *d_alpha, *d_rerr;
-    int *d_iota, *d_order, *d_pos, *d_npos, *d_feat, *d_count, *d_pid, *d_nid, *d_cnt, *d_lvl, *d_segoff;
-    int2 *d_leaves, *d_children, *d_brk;
-    void *d_tmp = nullptr;
-    size_t tmp_bytes = 0;
+    double *d_xs, *d_b, *d_xt, *d_xsorted, *d_y, *d_w, *d_err, *d_thr, *d_pol, *d_alpha, *d_rerr;
+    int *d_iota, *d_order, *d_pos, *d_npos, *d_feat, *d_count;
+    unsigned *d_code;
     int npos = 0;
     PwTree tree;
     int root = 0;
@@ -1069,7 +720,11 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
     BCU(S.get(&d_b, n));
     BCU(cudaMemcpyAsync(d_b, betas, sizeof(double) * n, cudaMemcpyDefault, s));
     BCU(S.get(&d_y, n));
-    BCU(S.get(&d_npos, 1));
+    if (out_n_pos && is_dev(out_n_pos)) {
+      d_npos = out_n_pos;
+    } else {
+      BCU(S.get(&d_npos, 1));
+    }
     BCU(cudaMemsetAsync(d_npos, 0, sizeof(int), s));
     {
       const int tok = prof_begin(PK_AUX, s);
@@ -1079,6 +734,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
     if (!dev_out) {  // (device results: the kernel itself handles one class)
       BCU(cudaMemcpyAsync(&npos, d_npos, sizeof(int), cudaMemcpyDeviceToHost, s));
       BCU(cudaStreamSynchronize(s));
+      if (out_n_pos && !is_dev(out_n_pos)) *out_n_pos = npos;
     }
     if (!dev_out && !raw && (npos == 0 || npos == n)) {
       // one class: zero-round ensemble carrying the class sign (boosting.py:185-187)
@@ -1089,32 +745,22 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
     BCU(S.get(&d_xt, (size_t)n * F));
     BCU(S.get(&d_xsorted, (size_t)n * F));
     BCU(S.get(&d_iota, (size_t)n * F));
-    BCU(S.get(&d_segoff, F + 1));
     BCU(S.get(&d_order, (size_t)n * F));
     {
       const int tok = prof_begin(PK_AUX, s);
       transpose_cols<<<(unsigned)(((int64_t)n * F + 255) / 256), 256, 0, s>>>(d_xs, n, F, d_xt, d_iota);
       prof_end(tok, s);
     }
-    // stable LSD radix sort of each column: ties keep index order, as np.argsort(kind="stable")
     {
-      // one segmented sort for all columns (segment f = column f)
-      std::vector<int> off(F + 1);
-      for (int f = 0; f <= F; ++f) off[f] = f * n;
-      BCU(cudaMemcpyAsync(d_segoff, off.data(), sizeof(int) * (F + 1), cudaMemcpyHostToDevice, s));
-      BCU(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp_bytes, d_xt, d_xsorted, d_iota, d_order, n * F, F,
-                                                   d_segoff, d_segoff + 1, 0, 64, s));
-      BCU(S.get(reinterpret_cast<char **>(&d_tmp), tmp_bytes));
-      BCU(cub::DeviceSegmentedRadixSort::SortPairs(d_tmp, tmp_bytes, d_xt, d_xsorted, d_iota, d_order, n * F, F,
-                                                   d_segoff, d_segoff + 1, 0, 64, s));
-    }
-    BCU(S.get(&d_pid, (size_t)n * F));
-    BCU(S.get(&d_nid, (size_t)n * F));
-    BCU(S.get(&d_cnt, (size_t)n * F));
-    BCU(S.get(&d_brk, (size_t)n * F));
-    {
+      // stable argsort of every column (np.argsort(kind="stable")), own kernel
+      unsigned long long *k0, *k1;
+      unsigned *i0, *i1;
+      BCU(S.get(&k0, (size_t)n * F));
+      BCU(S.get(&k1, (size_t)n * F));
+      BCU(S.get(&i0, (size_t)n * F));
+      BCU(S.get(&i1, (size_t)n * F));
       const int tok = prof_begin(PK_AUX, s);
-      split_classes<<<F, 256, 0, s>>>(d_order, d_y, d_xsorted, n, d_pid, d_nid, d_cnt, d_brk);
+      sort_columns<<<F, kSortThreads, 0, s>>>(d_xt, n, k0, i0, k1, i1, d_xsorted, d_order);
       prof_end(tok, s);
     }
     BCU(S.get(&d_w, n));
@@ -1125,12 +771,8 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       fill_value<<<(n + 255) / 256, 256, 0, s>>>(d_w, n, 1.0 / n);
       prof_end(tok, s);
     }
-    BCU(S.get(&d_wn, (size_t)n * F));
-    BCU(S.get(&d_pc, (size_t)n * F));
-    BCU(S.get(&d_nc, (size_t)n * F));
-    BCU(S.get(&d_err, F));
-    BCU(S.get(&d_pos, F));
-    BCU(S.get(&d_wsub, (size_t)n * F));
+    BCU(S.get(&d_err, 2 * F));
+    BCU(S.get(&d_pos, 2 * F));
     BCU(S.get(&d_feat, rounds));
     BCU(S.get(&d_thr, rounds));
     BCU(S.get(&d_pol, rounds));
@@ -1148,47 +790,75 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       d_count = out_count;
       d_icept = out_intercept;
     }
-    root = pw_tree(n, tree);
-    double *d_leafsum;
-    BCU(S.get(&d_leafsum, tree.leaves.size()));
-    BCU(S.get(&d_leaves, tree.leaves.size()));
-    BCU(cudaMemcpyAsync(d_leaves, tree.leaves.data(), sizeof(int2) * tree.leaves.size(), cudaMemcpyHostToDevice, s));
-    BCU(S.get(&d_children, tree.children.size()));
-    if (!tree.children.empty())
-      BCU(cudaMemcpyAsync(d_children, tree.children.data(), sizeof(int2) * tree.children.size(),
-                          cudaMemcpyHostToDevice, s));
-    BCU(S.get(&d_lvl, tree.level_end.size()));
-    if (!tree.level_end.empty())
-      BCU(cudaMemcpyAsync(d_lvl, tree.level_end.data(), sizeof(int) * tree.level_end.size(), cudaMemcpyHostToDevice,
+    if (mode == BRM_MODE_FAST) {
+      FastBoostParams Q{};
+      Q.n = n;
+      Q.F = F;
+      Q.rounds = rounds;
+      Q.raw = raw ? 1 : 0;
+      Q.xs = d_xs;
+      Q.xsorted = d_xsorted;
+      Q.y = d_y;
+      Q.order = d_order;
+      Q.w = d_w;
+      BCU(S.get(&Q.ysorted, (size_t)F * n));
+      BCU(S.get(&Q.wpart, F));
+      long long *d_ferr = nullptr;
+      BCU(S.get(&d_ferr, F));
+      Q.feat_err = d_ferr;
+      Q.feat_pos = d_pos;
+      Q.out_feat = d_feat;
+      Q.out_thr = d_thr;
+      Q.out_pol = d_pol;
+      Q.out_alpha = d_alpha;
+      Q.out_err = d_rerr;
+      Q.out_count = d_count;
+      Q.out_intercept = d_icept;
+      Q.n_pos = d_npos;
+      void *qargs[] = {&Q};
+      const int tok = prof_begin(PK_BOOST, s);
+      BCU(cudaLaunchCooperativeKernel((void *)boost_fast_kernel, dim3(F), dim3(kBoostThreads), qargs, 0, s));
+      prof_end(tok, s);
+    } else {
+      BCU(S.get(&d_code, (size_t)n * F));
+      {
+        const int tok = prof_begin(PK_AUX, s);
+        build_codes<<<dim3((n + 255) / 256, F), 256, 0, s>>>(d_order, d_y, d_xsorted, n, d_code);
+        prof_end(tok, s);
+      }
+      root = pw_tree(n, tree);
+      int2 *d_leaves, *d_children;
+      int *d_lvl;
+      BCU(S.get(&d_leaves, tree.leaves.size()));
+      BCU(cudaMemcpyAsync(d_leaves, tree.leaves.data(), sizeof(int2) * tree.leaves.size(), cudaMemcpyHostToDevice,
                           s));
-    {
-      BoostParams P{};
+      BCU(S.get(&d_children, std::max<size_t>(tree.children.size(), 1)));
+      if (!tree.children.empty())
+        BCU(cudaMemcpyAsync(d_children, tree.children.data(), sizeof(int2) * tree.children.size(),
+                            cudaMemcpyHostToDevice, s));
+      BCU(S.get(&d_lvl, std::max<size_t>(tree.level_end.size(), 1)));
+      if (!tree.level_end.empty())
+        BCU(cudaMemcpyAsync(d_lvl, tree.level_end.data(), sizeof(int) * tree.level_end.size(),
+                            cudaMemcpyHostToDevice, s));
+      CbParams P{};
       P.n = n;
       P.F = F;
       P.rounds = rounds;
       P.raw = raw ? 1 : 0;
-      P.xs = d_xs;
       P.xsorted = d_xsorted;
+      P.code = d_code;
       P.xt = d_xt;
       P.y = d_y;
-      P.w = d_w;
-      P.wn = d_wn;
-      P.pos_idx = d_pid;
-      P.neg_idx = d_nid;
-      P.cntpos = d_cnt;
-      P.brk = d_brk;
-      P.pcum = d_pc;
-      P.ncum = d_nc;
+      P.w0 = d_w;
       P.leaves = d_leaves;
       P.n_leaves = (int)tree.leaves.size();
       P.children = d_children;
       P.level_end = d_lvl;
       P.n_levels = (int)tree.level_end.size();
       P.root = root;
+      P.margin = 2 * (n + 64);
       P.feat_err = d_err;
       P.feat_pos = d_pos;
-      P.wsub = d_wsub;
-      P.leafsum = d_leafsum;
       P.out_feat = d_feat;
       P.out_thr = d_thr;
       P.out_pol = d_pol;
@@ -1197,65 +867,108 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       P.out_count = d_count;
       P.out_intercept = d_icept;
       P.n_pos = d_npos;
-      long long *d_timing = nullptr;
       const bool timing = getenv("BRM_BOOST_TIMING") != nullptr;
+      long long *d_timing = nullptr;
       if (timing) {
-        BCU(S.get(&d_timing, 12));
-        BCU(cudaMemsetAsync(d_timing, 0, 12 * sizeof(long long), s));
+        BCU(S.get(&d_timing, 16));
+        BCU(cudaMemsetAsync(d_timing, 0, 16 * sizeof(long long), s));
+        BCU(S.get(&P.n_fallback, 1));
+        BCU(cudaMemsetAsync(P.n_fallback, 0, sizeof(unsigned long long), s));
+        BCU(S.get(&P.n_events, 2));
+        BCU(cudaMemsetAsync(P.n_events, 0, 2 * sizeof(int), s));
       }
       P.timing = d_timing;
+      // cluster size: up to 8 CTAs per feature while every CTA of the
+      // cooperative grid stays co-resident (one cluster per feature)
+      int sms = 148;
+      BCU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      int cl = std::max(1, std::min(kCbMaxCluster, sms / F));
+      const int L = (int)tree.leaves.size();
+      // (slice_cap, pos_cap, dynamic shared memory) for cluster size c
+      auto layout = [&](int c, int &slice_cap, int &pos_cap) {
+        slice_cap = 0;
+        for (int r = 0; r < c; ++r) {
+          int lo, hi;
+          cb_leaf_run(L, c, r, lo, hi);
+          if (hi > lo) slice_cap = std::max(slice_cap, tree.leaves[hi - 1].x + tree.leaves[hi - 1].y - tree.leaves[lo].x);
+        }
+        slice_cap = std::max(slice_cap, 1);
+        // positions per thread: spread one tile evenly when it fits, else full tiles
+        const int qt = (int)std::min<int64_t>(kCbQ, ((int64_t)n + (int64_t)c * kCbThreads - 1) / ((int64_t)c * kCbThreads));
+        const int ctile = c * qt * kCbThreads;
+        pos_cap = (n + ctile - 1) / ctile * qt * kCbThreads;
+        return cb_smem_bytes(L, (int)tree.children.size(), (int)tree.level_end.size(), slice_cap, pos_cap);
+      };
       int smem_max = 0;
       BCU(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-      const size_t smem_cap = (size_t)smem_max - 2048;  // static shared arrays of the kernel
-      const size_t tree_bytes = sizeof(int2) * (tree.leaves.size() + tree.children.size()) +
-                                sizeof(int) * tree.level_end.size();
-      size_t smem = sizeof(double) * (2 * tree.leaves.size() + 4 * chain_padded_len(kTile));
-      P.tree_smem = smem + tree_bytes <= smem_cap ? 1 : 0;
-      if (P.tree_smem) smem += tree_bytes;
-      void *boost_fn = (void *)boost_kernel;
-      BCU(cudaFuncSetAttribute(boost_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      void *args[] = {&P};
-      const int tok = prof_begin(PK_BOOST, s);
-      if (mode == BRM_MODE_FAST) {
-        FastBoostParams Q{};
-        Q.n = n;
-        Q.F = F;
-        Q.rounds = rounds;
-        Q.raw = raw ? 1 : 0;
-        Q.xs = d_xs;
-        Q.xsorted = d_xsorted;
-        Q.y = d_y;
-        Q.order = d_order;
-        Q.w = d_w;
-        BCU(S.get(&Q.ysorted, (size_t)F * n));
-        BCU(S.get(&Q.wpart, F));
-        long long *d_ferr = nullptr;
-        BCU(S.get(&d_ferr, F));
-        Q.feat_err = d_ferr;
-        Q.feat_pos = d_pos;
-        Q.out_feat = d_feat;
-        Q.out_thr = d_thr;
-        Q.out_pol = d_pol;
-        Q.out_alpha = d_alpha;
-        Q.out_err = d_rerr;
-        Q.out_count = d_count;
-        Q.out_intercept = d_icept;
-        Q.n_pos = d_npos;
-        void *qargs[] = {&Q};
-        BCU(cudaLaunchCooperativeKernel((void *)boost_fast_kernel, dim3(F), dim3(kBoostThreads), qargs, 0, s));
-      } else {
-        BCU(cudaLaunchCooperativeKernel(boost_fn, dim3(F), dim3(kBoostThreads), args, smem, s));
+      int slice_cap = 0, pos_cap = 0;
+      size_t dyn = layout(cl, slice_cap, pos_cap);
+      while (cl < kCbMaxCluster && cl * 2 <= sms / F && dyn + sizeof(CbShared) + 2048 > (size_t)smem_max)
+        dyn = layout(++cl, slice_cap, pos_cap);  // (more CTAs -> smaller slices)
+      if (dyn + sizeof(CbShared) + 2048 > (size_t)smem_max) {
+        rc = bfail(BRM_EINVAL, "training set too large for the device AdaBoost's shared memory");
+        goto done;
       }
-      prof_end(tok, s);
+      BCU(cudaFuncSetAttribute((void *)boost_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+      cudaLaunchConfig_t lc{};
+      cudaLaunchAttribute at[2];
+      lc.blockDim = dim3(kCbThreads);
+      lc.dynamicSmemBytes = dyn;
+      lc.stream = s;
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      at[1].id = cudaLaunchAttributeClusterDimension;
+      at[1].val.clusterDim.y = 1;
+      at[1].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 2;
+      // every cluster must be resident at once (grid barrier)
+      for (;; --cl) {
+        dyn = layout(cl, slice_cap, pos_cap);
+        BCU(cudaFuncSetAttribute((void *)boost_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)dyn));
+        at[1].val.clusterDim.x = cl;
+        lc.gridDim = dim3((unsigned)(F * cl));
+        lc.dynamicSmemBytes = dyn;
+        int max_clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, (void *)boost_cluster_kernel, &lc) != cudaSuccess) {
+          cudaGetLastError();
+          max_clusters = 0;
+        }
+        if (max_clusters >= F || cl == 1) break;
+      }
+      P.cl = cl;
+      P.qt = (int)std::min<int64_t>(kCbQ, ((int64_t)n + (int64_t)cl * kCbThreads - 1) / ((int64_t)cl * kCbThreads));
+      P.slice_cap = slice_cap;
+      P.pos_cap = pos_cap;
+      double *d_fthr;
+      BCU(S.get(&d_fthr, 2 * F));
+      P.feat_thr = d_fthr;
+      BCU(S.get(&P.chain_g, (size_t)2 * n * F));
+      BCU(S.get(&P.wsub, (size_t)n * F * cl));
+      {
+        void *args[] = {&P};
+        const int tok = prof_begin(PK_BOOST, s);
+        BCU(cudaLaunchKernelExC(&lc, (void *)boost_cluster_kernel, args));
+        prof_end(tok, s);
+      }
       if (timing) {
-        long long h[12];
-        BCU(cudaMemcpyAsync(h, d_timing, sizeof h, cudaMemcpyDeviceToHost, s));
+        long long h[16];
+        unsigned long long fb = 0;
+        int ev[2];
+        BCU(cudaMemcpyAsync(h, d_timing, sizeof(long long) * 16, cudaMemcpyDeviceToHost, s));
+        BCU(cudaMemcpyAsync(&fb, P.n_fallback, sizeof fb, cudaMemcpyDeviceToHost, s));
+        BCU(cudaMemcpyAsync(ev, P.n_events, sizeof ev, cudaMemcpyDeviceToHost, s));
         BCU(cudaStreamSynchronize(s));
-        fprintf(stderr, "boost phases (kcycles, CTA 0): norm+total %.0f chains %.0f (positive chain alone %.0f) scan %.0f "
-                "sync1 %.0f pick %.0f reweight+sync2 %.0f (reweight alone %.0f)\n",
-                h[1] / 1e3, h[2] / 1e3, h[7] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, h[6] / 1e3, h[0] / 1e3);
-        fprintf(stderr, "  sub-phases (kcycles): [8] %.0f [9] %.0f [10] %.0f [11] %.0f\n", h[8] / 1e3, h[9] / 1e3,
-                h[10] / 1e3, h[11] / 1e3);
+        fprintf(stderr, "cluster boost (kcycles, cluster 0 CTA 0, %d rounds, %d x %d CTAs): chains %.0f "
+                "split-merge %.0f grid-sync %.0f pick+alpha %.0f reweight %.0f setup %.0f; events %d + %d; "
+                "fallback tiles %llu\n",
+                rounds, F, cl, h[0] / 1e3, h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, ev[0], ev[1],
+                fb);
+        fprintf(stderr, "  chain detail (kcycles): load+fpscan %.0f sync-d %.0f classify+scans %.0f sync-l %.0f "
+                "push %.0f sync-e %.0f walk %.0f sync-w %.0f | reweight: pass1 %.0f tree1 %.0f\n",
+                h[6] / 1e3, h[7] / 1e3, h[8] / 1e3, h[9] / 1e3, h[10] / 1e3, h[11] / 1e3, h[12] / 1e3, h[13] / 1e3,
+                h[14] / 1e3, h[15] / 1e3);
       }
     }
     BCU(cudaGetLastError());

@@ -791,7 +791,8 @@ int brm_normals(int32_t device, uint64_t key64, uint64_t stream64, uint64_t star
 
 int brm_selftest_math(int32_t device, int32_t kind, const double *a, const double *b, int64_t n, double *out) {
   if (n <= 0) return BRM_OK;
-  if (kind < 0 || kind > 9) return fail(BRM_EINVAL, "unknown self-test %d", kind);
+  if (kind < 0 || kind > 10 || kind == 9) return fail(BRM_EINVAL, "unknown self-test %d", kind);
+  if (kind == 10 && n > (1 << 30)) return fail(BRM_EINVAL, "exact-scan self-test too long");
   if (kind >= 8 && n > 2147483647LL) return fail(BRM_EINVAL, "chain self-test too long");
   DeviceScope scope(device);
   Call call(nullptr);
@@ -801,7 +802,15 @@ int brm_selftest_math(int32_t device, int32_t kind, const double *a, const doubl
   if (kind == 2 || kind == 3) BRM_TRY(call.in(b, n, &db));
   BRM_TRY(call.out(out, n, &o));
   void *args[] = {&kind, &da, &db, &n, &o};
-  if (kind >= 8) {
+  if (kind == 10) {
+    unsigned *code;
+    double *chain;
+    BRM_TRY(call.scratch(n, &code));
+    BRM_TRY(call.scratch(2 * n, &chain));
+    int ni = (int)n;
+    void *eargs[] = {&da, &ni, &code, &chain, &o};
+    BRM_CUDA(cudaLaunchKernel(exact_scan_selftest_kernel(), dim3(1), dim3(512), eargs, 0, call.stream));
+  } else if (kind >= 8) {
     void *cargs[] = {&kind, &da, &n, &o};
     BRM_CUDA(cudaLaunchKernel(chain_selftest_kernel(), dim3(1), dim3(32), cargs, 0, call.stream));
   } else {

@@ -120,6 +120,7 @@ void *fill_raw_kernel();
 void *fill_normals_kernel();
 void *math_selftest_kernel();
 void *chain_selftest_kernel();
+void *exact_scan_selftest_kernel();
 // Slotted CMC images (brm_ctx_create_cmc): per date, `ts` threshold entries
 // and `vs` table values.  Each feature's padded threshold list has at most
 // 2 u_f entries (u_f distinct thresholds, padded to a power of two minus one)

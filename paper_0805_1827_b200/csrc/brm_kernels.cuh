@@ -136,7 +136,6 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
   const int probe = blockIdx.x / csize;
 
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double s_red[2 * (kWalkThreads / 32)];
   __shared__ int s_next;
   __shared__ R s_start[kMaxD];
   __shared__ double s_state[kMaxD];

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 def test_python_binding_covers_the_header():
     from paper_0805_1827_b200 import _native as N
     assert set(declared_functions()) == set(N.SYMBOLS)
-    assert N.lib.brm_abi_version() == N.ABI_VERSION == 2
+    assert N.lib.brm_abi_version() == N.ABI_VERSION == 3
 
 
 def test_errors_map_to_reference_exceptions_without_a_gpu():

@@ -289,8 +289,8 @@ def test_branch_free_math_is_bit_identical():
     assert np.array_equal(run(6, s).view(np.int64), run(7, s).view(np.int64))
 
 
-def test_warp_chain_is_bit_identical_to_sequential_cumsum():
-    """AdaBoost's warp-parallel binade-tile prefix sums (brm_chain.cuh) equal the one-thread
+def test_exact_scan_is_bit_identical_to_sequential_cumsum():
+    """AdaBoost's block-parallel exact scan (brm_boost_exact.cuh, kind 10) equals the one-thread
     sequential np.cumsum chain bit for bit: AdaBoost-like weights, wide dynamic ranges, zeros,
     exact ties (dyadic weights), long and short chains."""
     from paper_0805_1827_b200 import _native as N
@@ -316,8 +316,8 @@ def test_warp_chain_is_bit_identical_to_sequential_cumsum():
     cases.append(np.sort(rng.random(5000))[::-1].copy())           # decreasing
     for a in cases:
         a = np.ascontiguousarray(a)
-        seq, war = run(8, a), run(9, a)
-        assert np.array_equal(seq.view(np.int64), war.view(np.int64)), a.size
+        seq, ex = run(8, a), run(10, a)
+        assert np.array_equal(seq.view(np.int64), ex.view(np.int64)), a.size
         assert np.array_equal(seq, np.cumsum(a))
 
 
