@@ -226,6 +226,19 @@ int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, void *stream, 
                      int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha, double *out_err,
                      int32_t *out_count, double *out_intercept, int32_t *out_n_pos);
 
+/* ---- Device-resident I&Z date step (boundary_iz.py:328-357) ------------- */
+/* Fit date m's boundary surface(s) on the device and write them into the
+ * context's rule image, ordered on the context's stream (no host round trip:
+ * the next, earlier date's brm_iz_solve on the same context uses them).
+ * design [J*nb] row-major quadratic basis of k_coords coordinates (host or
+ * device); levels [n_fits*J] (host or device; their logs for a log-space
+ * surface); n_fits = d for price surfaces (fit g is asset g's surface), 1 for
+ * the log-space surface (written to every row).  Rank-deficient designs fall
+ * back to the cross-term-free basis as brm_lstsq.  out_coeffs [n_fits*nb] and
+ * out_rank [n_fits] are optional (NULL), host or device. */
+int brm_iz_fit(brm_ctx *ctx, int32_t m, const double *design, int32_t J, int32_t nb, int32_t k_coords,
+               const double *levels, int32_t n_fits, int32_t log_space, double *out_coeffs, int32_t *out_rank);
+
 /* ---- Quadratic boundary regression (boundary_iz.py:250-276) ------------- */
 /* Least squares over the design [n*nb] (row-major), fp64 Householder QR with
  * column pivoting on the device; rank-deficient designs fall back to the

@@ -86,6 +86,8 @@ _SIGNATURES = {
     "brm_transfer_read": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "brm_lstsq": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                             C.c_void_p, _ip]),
+    "brm_iz_fit": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                             C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
 }
 
 

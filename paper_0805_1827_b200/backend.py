@@ -99,16 +99,29 @@ def decisions(mp, rp, states, m: int, mode=None, device=None, ctx=None) -> np.nd
 def iz_solve_batch(mp, rp, seeds, assets, m: int, n_inner: int, *, solver: str = "fixed_point",
                    epsilon: float = 0.01, max_iter: int = 100, avg_window: int = 5,
                    lo: float = 0.0, hi: float = 0.0, tol: float = 1e-4, keys=None, streams=None,
-                   seed: int = 0, item_lo: int = 0, mode=None, device=None):
-    """Solve n probes at date m; returns (levels, iterations, converged)."""
-    ctx = get_context(mp, rp, device, mode)
+                   seed: int = 0, item_lo: int = 0, mode=None, device=None, ctx=None, out=None):
+    """Solve n probes at date m; returns (levels, iterations, converged).
+
+    ``ctx`` overrides the context of (mp, rp); ``seeds`` / ``assets`` may be
+    device tensors and ``out`` a (levels f64, iterations i32, converged i32)
+    triple of device tensors, which are then filled without a host round trip."""
+    ctx = get_context(mp, rp, device, mode) if ctx is None else ctx
     d = int(mp.d)
-    assets = np.ascontiguousarray(assets, dtype=np.int32)
-    n = assets.size
-    seeds = N.f64(seeds).reshape(n, max(d - 1, 0)) if d > 1 else np.zeros((n, 0))
-    levels = np.empty(n)
-    its = np.empty(n, dtype=np.int32)
-    conv = np.empty(n, dtype=np.int32)
+    if isinstance(assets, np.ndarray) or not hasattr(assets, "data_ptr"):
+        assets = np.ascontiguousarray(assets, dtype=np.int32)
+        n = assets.size
+    else:
+        n = int(assets.shape[0])
+    if d > 1:
+        seeds = N.f64(seeds).reshape(n, d - 1) if not hasattr(seeds, "data_ptr") else seeds
+    else:
+        seeds = np.zeros((n, 0))
+    if out is not None:
+        levels, its, conv = out
+    else:
+        levels = np.empty(n)
+        its = np.empty(n, dtype=np.int32)
+        conv = np.empty(n, dtype=np.int32)
     kp = sp = None
     if keys is not None:
         kp = np.ascontiguousarray(keys, dtype=np.uint64)
@@ -118,6 +131,8 @@ def iz_solve_batch(mp, rp, seeds, assets, m: int, n_inner: int, *, solver: str =
                                int(n_inner), float(epsilon), int(max_iter), int(avg_window), float(lo), float(hi),
                                float(tol), N.ptr(kp), N.ptr(sp), int(seed) & (2**64 - 1), int(item_lo),
                                N.ptr(levels), N.ptr(its), N.ptr(conv)))
+    if out is not None:
+        return levels, its, conv
     return levels, its, conv.astype(bool)
 
 

@@ -202,11 +202,98 @@ def _default_bracket(spec, iz_space: int, call_like: bool, lo_mult: float, hi_mu
     return K, hi_mult * K
 
 
+def _torch_cuda():
+    try:
+        import torch
+        return torch if torch.cuda.is_available() else None
+    except ImportError:
+        return None
+
+
+def _build_device_loop(params, spec, n_inner, epsilon, max_iter, seed, solver, lo_b, hi_b, tol, mode, shard, torch,
+                       mp, d, call_like, iz_space, box, reg_pts, assets_per_item, item_asset, item_seed, j_points,
+                       report):
+    """The backward date loop with no host round trip until the end: per date
+    the probe clusters write their levels to HBM, the level exchange is a
+    device collective, and brm_iz_fit regresses the surface(s) on the device
+    straight into the rule image the next (earlier) date's probes read.
+    Per-date times are CUDA-event times on torch's current stream."""
+    from .context import Context
+    nd = spec.n_dates
+    stream = torch.cuda.current_stream()
+    boundary0 = IzBoundary.terminal_only(spec, d, box, iz_space)
+    ctx = Context(mp, boundary0.pack(), mode=mode)  # private image, surfaces filled date by date
+    ctx.set_stream(stream)
+    f64, i32 = torch.float64, torch.int32
+    pts = np.log(reg_pts) if iz_space == 1 else reg_pts
+    design_h = quad_basis(pts) if pts.shape[1] else np.ones((j_points, 1))
+    J, nb = design_h.shape
+    if J < nb:
+        raise ConfigError(f"need at least {nb} probe points for the quadratic fit, got {J}")
+    n_items = item_asset.size
+    n_fits = 1 if iz_space == 1 else d
+    design = torch.from_numpy(np.ascontiguousarray(design_h)).to("cuda")
+    seeds_dev = torch.from_numpy(np.ascontiguousarray(item_seed, dtype=np.float64)).to("cuda")
+    assets_dev = torch.from_numpy(np.ascontiguousarray(item_asset, dtype=np.int32)).to("cuda")
+    levels = torch.zeros((nd + 1, n_items), dtype=f64, device="cuda")
+    iters = torch.zeros((nd + 1, n_items), dtype=i32, device="cuda")
+    conv = torch.zeros((nd + 1, n_items), dtype=i32, device="cuda")
+    coeffs = torch.zeros((nd + 1, n_fits, nb), dtype=f64, device="cuda")
+    ranks = torch.zeros((nd + 1, n_fits), dtype=i32, device="cuda")
+    marks = []
+    for m in range(nd - 1, 0, -1):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        for lo, hi in shard.local_ranges(n_items):
+            if hi > lo:
+                _be.iz_solve_batch(mp, None, seeds_dev[lo:hi] if d > 1 else None, assets_dev[lo:hi], m, n_inner,
+                                   solver=solver, epsilon=epsilon, max_iter=max_iter, avg_window=5, lo=lo_b, hi=hi_b,
+                                   tol=tol, seed=seed, item_lo=lo, mode=mode, ctx=ctx,
+                                   out=(levels[m, lo:hi], iters[m, lo:hi], conv[m, lo:hi]))
+        if shard.distributed:  # disjoint rows, zero elsewhere: the sum is an exact gather
+            for t in (levels[m], iters[m], conv[m]):
+                shard.all_reduce_sum(t)
+        ev[1].record(stream)
+        # levels[m] is [n_fits * J]: fit g regresses asset g's probes (one fit in log space)
+        ctx.iz_fit(m, design, J, nb, pts.shape[1], levels[m], n_fits, iz_space == 1, coeffs[m], ranks[m])
+        ev[2].record(stream)
+        marks.append((m, ev))
+    host = {"levels": levels.cpu().numpy(), "iters": iters.cpu().numpy(), "conv": conv.cpu().numpy(),
+            "coeffs": coeffs.cpu().numpy(), "ranks": ranks.cpu().numpy()}  # the build's one synchronisation
+    ctx.close()
+    full = boundary0.coeffs.copy()
+    for m, ev in marks:
+        if iz_space == 1:
+            full[m, :] = host["coeffs"][m, 0]
+        else:
+            for a_idx, asset in enumerate(assets_per_item):
+                full[m, asset] = host["coeffs"][m, a_idx]
+        if np.any(host["ranks"][m] < nb):
+            import warnings
+            warnings.warn("rank-deficient boundary design; dropping cross terms")
+        its = host["iters"][m].astype(int)
+        n_unconv = int(np.sum(host["conv"][m] == 0))
+        calc_s, reg_s = ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3
+        report.calc_seconds += calc_s
+        report.reg_seconds += reg_s
+        report.unconverged_points += n_unconv
+        report.iteration_counts.extend(its.tolist())
+        report.per_date.append({"date_index": m, "calc_seconds": calc_s, "reg_seconds": reg_s,
+                                "unconverged": n_unconv, "iterations": its.tolist()})
+    report.per_date.reverse()
+    return IzBoundary(spec.strike, d, nd, call_like, full, box, iz_space), report
+
+
 def build_iz_boundary(params, spec, j_points: int, n_inner: int, epsilon: float = 0.01, max_iter: int = 100,
                       seed: int = 0, engine=None, lo_mult: float = 0.5, hi_mult: float = 2.5, backend=None, *,
                       solver: str = "fixed_point", bracket=None, tol: float = 1e-4, grid: str | None = None,
-                      mode=None) -> tuple[IzBoundary, IzBuildReport]:
-    """Backward induction over dates (boundary_iz.py:296-360)."""
+                      mode=None, device_loop=None) -> tuple[IzBoundary, IzBuildReport]:
+    """Backward induction over dates (boundary_iz.py:296-360).
+
+    device_loop: keep the date loop on the device (default when a GPU is
+    visible): probe levels, the level exchange and the regression stay in
+    HBM and the surfaces are written into the rule image without a host
+    round trip; False regresses each date on the host path (brm_lstsq)."""
     spec.validate_against(params)
     code = payoff_code(spec.payoff_kind)
     d = params.d
@@ -238,6 +325,15 @@ def build_iz_boundary(params, spec, j_points: int, n_inner: int, epsilon: float 
     item_seed = np.tile(seeds, (len(assets_per_item), 1))
     lo_b, hi_b = bracket if bracket is not None else _default_bracket(spec, iz_space, call_like, lo_mult, hi_mult)
     mp = pack_market(params, spec)
+    torch = _torch_cuda()
+    if device_loop is None:
+        device_loop = torch is not None
+    if device_loop:
+        if torch is None:
+            raise RuntimeError("device_loop=True needs a CUDA device")
+        return _build_device_loop(params, spec, n_inner, epsilon, max_iter, seed, solver, lo_b, hi_b, tol, mode,
+                                  shard, torch, mp, d, call_like, iz_space, box, reg_grid.points, assets_per_item,
+                                  item_asset, item_seed, j_points, report)
     for m in range(spec.n_dates - 1, 0, -1):
         later = boundary.pack()
         t0 = time.perf_counter()

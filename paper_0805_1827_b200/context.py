@@ -103,6 +103,13 @@ class Context:
         N.check(N.lib.brm_ctx_set_ensemble(self.handle, int(m), N.ptr(feat), N.ptr(thr), N.ptr(pol), N.ptr(alpha),
                                            N.ptr(count), N.ptr(intercept)))
 
+    def iz_fit(self, m: int, design, J: int, nb: int, k_coords: int, levels, n_fits: int, log_space: bool,
+               out_coeffs=None, out_rank=None) -> None:
+        """Fit date m's boundary surface(s) on the device into this image
+        (brm_iz_fit): no host round trip when the arrays are device tensors."""
+        N.check(N.lib.brm_iz_fit(self.handle, int(m), N.ptr(design), int(J), int(nb), int(k_coords), N.ptr(levels),
+                                 int(n_fits), 1 if log_space else 0, N.ptr(out_coeffs), N.ptr(out_rank)))
+
     def close(self) -> None:
         self._finalizer()
 

@@ -536,44 +536,41 @@ __global__ void fill_value(double *w, int n, double v) {
 }
 
 // --------------------------------------------------------------- lstsq ----
-// Householder QR with column pivoting in one CTA (fp64).  Returns rank.
-constexpr int kLsMaxN = 4096, kLsMaxB = 64;
+// Quadratic boundary regression (boundary_iz.py:250-276) on the device:
+// Householder QR with column pivoting in one CTA per fit (fp64), the
+// rank-deficient fallback to the cross-term-free basis inside the kernel.
+// Fit g solves design[J x nb] (shared) against levels[g*J .. g*J+J) (their
+// logs in log space), writes its coefficients to out[g*nb ..], its rank to
+// rank_out[g], and -- for the device-resident I&Z date loop -- into the rule
+// image: rows dst[g*row_stride + (0 .. rows-1)*nb] of the surface block.
+__device__ __forceinline__ double ls_warp_sum(double s) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
+}
 
-__global__ void lstsq_kernel(const double *design, const double *levels, int n, int nb, const int *cols, int ncols,
-                             double *coeffs, int *rank_out) {
-  extern __shared__ double sm[];
-  double *A = sm;                       // [ncols][n] column-major
-  double *b = A + (size_t)ncols * n;    // [n]
-  __shared__ double s_norm[kLsMaxB];
-  __shared__ int s_perm[kLsMaxB];
-  __shared__ double s_tau, s_beta, s_r00;
-  __shared__ int s_rank;
-  for (int i = threadIdx.x; i < n * ncols; i += blockDim.x) {
-    const int c = i / n, r = i % n;
-    A[i] = design[(size_t)r * nb + cols[c]];
-  }
-  for (int r = threadIdx.x; r < n; r += blockDim.x) b[r] = levels[r];
+// QR least squares over the design columns cols[0..ncols) of A (column-major,
+// [ncols][n] in shared memory, overwritten) and b; returns the rank, x in x[].
+__device__ int ls_solve(double *A, double *b, int n, int ncols, int *s_perm, double *s_norm, double *x,
+                        double *s_scal) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if (threadIdx.x < ncols) s_perm[threadIdx.x] = threadIdx.x;
-  if (threadIdx.x == 0) s_rank = 0;
   __syncthreads();
+  int rank = 0;
+  double r00 = 0.0;
   const int kmax = min(n, ncols);
   for (int k = 0; k < kmax; ++k) {
-    // column norms of the trailing block, pick the largest
-    for (int c = k + (threadIdx.x >> 5); c < ncols; c += blockDim.x >> 5) {
+    // column norms of the trailing block; the largest is the pivot
+    for (int c = k + warp; c < ncols; c += nw) {
       double s = 0.0;
-      for (int r = k + (threadIdx.x & 31); r < n; r += 32) s += A[(size_t)c * n + r] * A[(size_t)c * n + r];
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
-      if ((threadIdx.x & 31) == 0) s_norm[c] = s;
+      for (int r = k + lane; r < n; r += 32) s += A[(size_t)c * n + r] * A[(size_t)c * n + r];
+      s = ls_warp_sum(s);
+      if (lane == 0) s_norm[c] = s;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int best = k;
-      for (int c = k + 1; c < ncols; ++c)
-        if (s_norm[c] > s_norm[best]) best = c;
-      s_beta = best;
-    }
-    __syncthreads();
-    const int piv = (int)s_beta;
+    int piv = k;
+    for (int c = k + 1; c < ncols; ++c)
+      if (s_norm[c] > s_norm[piv]) piv = c;
     if (piv != k) {
       for (int r = threadIdx.x; r < n; r += blockDim.x) {
         const double t = A[(size_t)k * n + r];
@@ -587,51 +584,121 @@ __global__ void lstsq_kernel(const double *design, const double *levels, int n, 
       }
     }
     __syncthreads();
-    // Householder vector for column k
-    if (threadIdx.x == 0) {
-      double nrm = 0.0;
-      for (int r = k; r < n; ++r) nrm += A[(size_t)k * n + r] * A[(size_t)k * n + r];
-      nrm = sqrt(nrm);
+    // Householder vector of column k (warp 0), then its scaling (all threads)
+    if (warp == 0) {
+      double s = 0.0;
+      for (int r = k + lane; r < n; r += 32) s += A[(size_t)k * n + r] * A[(size_t)k * n + r];
+      const double nrm = sqrt(ls_warp_sum(s));
       const double x0 = A[(size_t)k * n + k];
       const double alpha = x0 >= 0.0 ? -nrm : nrm;
-      if (k == 0) s_r00 = fabs(alpha);
-      const double tol = (double)max(n, ncols) * 2.220446049250313e-16 * s_r00;
-      if (!(fabs(alpha) > tol) || nrm == 0.0) {
-        s_tau = 0.0;
-      } else {
-        s_rank = k + 1;
-        const double v0 = x0 - alpha;
-        A[(size_t)k * n + k] = alpha;
-        for (int r = k + 1; r < n; ++r) A[(size_t)k * n + r] /= v0;
-        s_tau = -v0 / alpha;  // H = I - tau v v^T with v = [1, A[k+1..n)]
+      if (k == 0) r00 = fabs(alpha);
+      const double tol = (double)max(n, ncols) * 2.220446049250313e-16 * (k == 0 ? fabs(alpha) : s_scal[2]);
+      if (lane == 0) {
+        if (k == 0) s_scal[2] = fabs(alpha);
+        if (!(fabs(alpha) > tol) || nrm == 0.0) {
+          s_scal[0] = 0.0;
+        } else {
+          s_scal[0] = -(x0 - alpha) / alpha;  // tau: H = I - tau v v^T, v = [1, A[k+1..n) / v0]
+          s_scal[1] = x0 - alpha;             // v0
+          A[(size_t)k * n + k] = alpha;
+        }
       }
     }
     __syncthreads();
-    const double tau = s_tau;
+    const double tau = s_scal[0];
     if (tau == 0.0) break;
-    // apply H to trailing columns and b
-    for (int c = k + 1 + (threadIdx.x >> 5); c <= ncols; c += blockDim.x >> 5) {
+    rank = k + 1;
+    const double v0 = s_scal[1];
+    for (int r = k + 1 + threadIdx.x; r < n; r += blockDim.x) A[(size_t)k * n + r] /= v0;
+    __syncthreads();
+    // apply H to the trailing columns and b (a warp per column)
+    for (int c = k + 1 + warp; c <= ncols; c += nw) {
       double *col = c < ncols ? A + (size_t)c * n : b;
       double s = 0.0;
-      for (int r = k + (threadIdx.x & 31); r < n; r += 32) s += (r == k ? 1.0 : A[(size_t)k * n + r]) * col[r];
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
-      s = __shfl_sync(0xffffffffu, s, 0) * tau;
-      for (int r = k + (threadIdx.x & 31); r < n; r += 32) col[r] -= s * (r == k ? 1.0 : A[(size_t)k * n + r]);
+      for (int r = k + lane; r < n; r += 32) s += (r == k ? 1.0 : A[(size_t)k * n + r]) * col[r];
+      s = ls_warp_sum(s) * tau;
+      for (int r = k + lane; r < n; r += 32) col[r] -= s * (r == k ? 1.0 : A[(size_t)k * n + r]);
     }
     __syncthreads();
   }
+  (void)r00;
   if (threadIdx.x == 0) {
-    const int rk = s_rank;
-    *rank_out = rk;
-    double x[kLsMaxB];
-    for (int i = rk - 1; i >= 0; --i) {
+    double y[kLsMaxB];
+    for (int i = rank - 1; i >= 0; --i) {
       double s = b[i];
-      for (int j = i + 1; j < rk; ++j) s -= A[(size_t)j * n + i] * x[j];
-      x[i] = s / A[(size_t)i * n + i];
+      for (int j = i + 1; j < rank; ++j) s -= A[(size_t)j * n + i] * y[j];
+      y[i] = s / A[(size_t)i * n + i];
     }
-    for (int c = 0; c < nb; ++c) coeffs[c] = 0.0;
-    for (int i = 0; i < rk; ++i) coeffs[cols[s_perm[i]]] = x[i];
+    for (int c = 0; c < ncols; ++c) x[c] = 0.0;
+    for (int i = 0; i < rank; ++i) x[s_perm[i]] = y[i];
   }
+  __syncthreads();
+  return rank;
+}
+
+__global__ void __launch_bounds__(256) ls_fit_kernel(LsParams P) {
+  extern __shared__ double sm[];
+  const int n = P.J, nb = P.nb, g = blockIdx.x;
+  double *A = sm;                      // [nb][n] column-major
+  double *b = A + (size_t)nb * n;      // [n]
+  __shared__ double s_norm[kLsMaxB], s_x[kLsMaxB], s_scal[4];
+  __shared__ int s_perm[kLsMaxB], s_cols[kLsMaxB];
+  const double *lv = P.levels + (size_t)g * n;
+  for (int i = threadIdx.x; i < n * nb; i += blockDim.x) {
+    const int c = i / n, r = i % n;
+    A[i] = P.design[(size_t)r * nb + c];
+  }
+  for (int r = threadIdx.x; r < n; r += blockDim.x) b[r] = P.log_space ? log(lv[r]) : lv[r];
+  __syncthreads();
+  int rank = ls_solve(A, b, n, nb, s_perm, s_norm, s_x, s_scal);
+  double coef[kLsMaxB];
+  for (int c = 0; c < nb; ++c) coef[c] = s_x[c];
+  const int rank_full = rank;
+  if (rank < nb) {
+    // keep [1, z_a, z_a^2], zero the cross terms (boundary_iz.py:264-275)
+    if (threadIdx.x == 0) {
+      int q = 0, pos = 1 + P.k;
+      s_cols[q++] = 0;
+      for (int a = 1; a <= P.k; ++a) s_cols[q++] = a;
+      for (int a = 0; a < P.k; ++a) {
+        s_cols[q++] = pos;
+        pos += P.k - a;
+      }
+    }
+    __syncthreads();
+    const int nk = 1 + 2 * P.k;
+    for (int i = threadIdx.x; i < n * nk; i += blockDim.x) {
+      const int c = i / n, r = i % n;
+      A[i] = P.design[(size_t)r * nb + s_cols[c]];
+    }
+    for (int r = threadIdx.x; r < n; r += blockDim.x) b[r] = P.log_space ? log(lv[r]) : lv[r];
+    __syncthreads();
+    ls_solve(A, b, n, nk, s_perm, s_norm, s_x, s_scal);
+    for (int c = 0; c < nb; ++c) coef[c] = 0.0;
+    for (int c = 0; c < nk; ++c) coef[s_cols[c]] = s_x[c];
+  }
+  if (threadIdx.x == 0) {
+    if (P.out)
+      for (int c = 0; c < nb; ++c) P.out[(size_t)g * nb + c] = coef[c];
+    if (P.rank_out) P.rank_out[g] = rank_full;
+    if (P.dst)
+      for (int row = 0; row < P.dst_rows; ++row)
+        for (int c = 0; c < nb; ++c) P.dst[(size_t)g * P.dst_fit_stride + (size_t)row * nb + c] = coef[c];
+  }
+}
+
+size_t ls_fit_smem(int J, int nb) { return sizeof(double) * ((size_t)nb * J + J); }
+
+int launch_ls_fit(const LsParams &P, int n_fits, cudaStream_t s) {
+  const size_t smem = ls_fit_smem(P.J, P.nb);
+  cudaError_t e = cudaFuncSetAttribute(ls_fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return set_error(BRM_ECUDA, "ls_fit: %s", cudaGetErrorString(e));
+  const int tok = prof_begin(PK_LSTSQ, s);
+  ls_fit_kernel<<<n_fits, 256, smem, s>>>(P);
+  prof_end(tok, s);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(BRM_ECUDA, "ls_fit launch: %s", cudaGetErrorString(e));
+  return BRM_OK;
 }
 
 }  // namespace brm
@@ -1014,63 +1081,33 @@ extern "C" int brm_lstsq(int32_t device, void *stream, const double *design, con
   cudaSetDevice(device);
   retain_pool(device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // one device block: [coeffs nb][rank 1 (as int, in a double slot)][design n*nb][levels n][cols nb (int)],
-  // so the full-rank case costs one allocation, one result copy and one sync
+  // one device block: [coeffs nb][rank (int, in a double slot)][design n*nb][levels n]
   unsigned char *blk = nullptr;
-  std::vector<int> cols(nb);
-  double hres[kLsMaxB + 1];  // coeffs, then the rank (an int) in the next slot
-  int rank = 0;
-  for (int c = 0; c < nb; ++c) cols[c] = c;
-  const size_t smem_full = sizeof(double) * ((size_t)nb * n + n);
+  double hres[kLsMaxB + 1];
   const size_t off_rank = sizeof(double) * nb;
   const size_t off_design = off_rank + sizeof(double);
   const size_t off_levels = off_design + sizeof(double) * (size_t)n * nb;
-  const size_t off_cols = off_levels + sizeof(double) * n;
-  const size_t blk_bytes = off_cols + sizeof(int) * nb;
-  double *d_coeffs, *d_design, *d_levels;
-  int *d_rank, *d_cols;
+  const size_t blk_bytes = off_levels + sizeof(double) * n;
+  LsParams P{};
   BCU(cudaMallocAsync(&blk, blk_bytes, s));
-  d_coeffs = reinterpret_cast<double *>(blk);
-  d_rank = reinterpret_cast<int *>(blk + off_rank);
-  d_design = reinterpret_cast<double *>(blk + off_design);
-  d_levels = reinterpret_cast<double *>(blk + off_levels);
-  d_cols = reinterpret_cast<int *>(blk + off_cols);
-  BCU(cudaMemcpyAsync(d_design, design, sizeof(double) * (size_t)n * nb, cudaMemcpyDefault, s));
-  BCU(cudaMemcpyAsync(d_levels, levels, sizeof(double) * n, cudaMemcpyDefault, s));
-  BCU(cudaMemcpyAsync(d_cols, cols.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, s));
-  BCU(cudaFuncSetAttribute(lstsq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
-  {
-    const int tok = prof_begin(PK_LSTSQ, s);
-    lstsq_kernel<<<1, 256, smem_full, s>>>(d_design, d_levels, n, nb, d_cols, nb, d_coeffs, d_rank);
-    prof_end(tok, s);
-  }
-  BCU(cudaGetLastError());
+  BCU(cudaMemcpyAsync(blk + off_design, design, sizeof(double) * (size_t)n * nb, cudaMemcpyDefault, s));
+  BCU(cudaMemcpyAsync(blk + off_levels, levels, sizeof(double) * n, cudaMemcpyDefault, s));
+  P.design = reinterpret_cast<const double *>(blk + off_design);
+  P.levels = reinterpret_cast<const double *>(blk + off_levels);
+  P.J = n;
+  P.nb = nb;
+  P.k = k;
+  P.out = reinterpret_cast<double *>(blk);
+  P.rank_out = reinterpret_cast<int *>(blk + off_rank);
+  if ((rc = launch_ls_fit(P, 1, s)) != BRM_OK) goto done;
   BCU(cudaMemcpyAsync(hres, blk, off_rank + sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (is_dev(out_coeffs)) BCU(cudaMemcpyAsync(out_coeffs, blk, sizeof(double) * nb, cudaMemcpyDeviceToDevice, s));
   BCU(cudaStreamSynchronize(s));
-  std::memcpy(&rank, reinterpret_cast<unsigned char *>(hres) + off_rank, sizeof(int));
-  *out_rank_deficient = rank < nb;
-  if (rank < nb) {
-    // keep [1, z_a, z_a^2], zero the cross terms (boundary_iz.py:264-275)
-    std::vector<int> keep{0};
-    for (int a = 1; a <= k; ++a) keep.push_back(a);
-    int pos = 1 + k;
-    for (int a = 0; a < k; ++a) {
-      keep.push_back(pos);
-      pos += k - a;
-    }
-    BCU(cudaMemcpyAsync(d_cols, keep.data(), sizeof(int) * keep.size(), cudaMemcpyHostToDevice, s));
-    const int tok = prof_begin(PK_LSTSQ, s);
-    lstsq_kernel<<<1, 256, sizeof(double) * (keep.size() * n + n), s>>>(d_design, d_levels, n, nb, d_cols,
-                                                                        (int)keep.size(), d_coeffs, d_rank);
-    prof_end(tok, s);
-    BCU(cudaGetLastError());
-    BCU(cudaMemcpyAsync(hres, blk, off_rank, cudaMemcpyDeviceToHost, s));
-    BCU(cudaStreamSynchronize(s));
-  }
-  if (is_dev(out_coeffs)) {
-    BCU(cudaMemcpyAsync(out_coeffs, d_coeffs, sizeof(double) * nb, cudaMemcpyDeviceToDevice, s));
-  } else {
-    std::memcpy(out_coeffs, hres, sizeof(double) * nb);
+  {
+    int rank = 0;
+    std::memcpy(&rank, reinterpret_cast<unsigned char *>(hres) + off_rank, sizeof(int));
+    *out_rank_deficient = rank < nb;
+    if (!is_dev(out_coeffs)) std::memcpy(out_coeffs, hres, sizeof(double) * nb);
   }
 done:
   if (blk) {

@@ -10,6 +10,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cmath>
+#include <map>
+#include <tuple>
 #include <limits>
 #include <cstring>
 #include <mutex>
@@ -182,6 +184,31 @@ int fetch(const T *src, size_t count, std::vector<T> &dst, const char *name) {
 }
 
 int quad_basis_size(int k) { return 1 + k + k * (k + 1) / 2; }
+
+// cudaOccupancyMaxActiveClusters, cached per (kernel, cluster size, block,
+// dynamic shared memory, device): the query costs tens of microseconds and
+// the per-date probe launches would repeat it.
+int max_active_clusters(const void *kernel, const cudaLaunchConfig_t &cfg, int device) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void *, int, int, size_t, int>, int> cache;
+  int csize = 1;
+  for (unsigned i = 0; i < cfg.numAttrs; ++i)
+    if (cfg.attrs[i].id == cudaLaunchAttributeClusterDimension) csize = (int)cfg.attrs[i].val.clusterDim.x;
+  const auto key = std::make_tuple(kernel, csize, (int)cfg.blockDim.x, cfg.dynamicSmemBytes, device);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  int v = 0;
+  if (cudaOccupancyMaxActiveClusters(&v, kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    v = 0;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = v;
+  return v;
+}
 
 }  // namespace
 
@@ -693,6 +720,42 @@ void retire_user_stream(brm_ctx *c) {
 }
 }  // namespace
 
+int brm_iz_fit(brm_ctx *c, int32_t m, const double *design, int32_t J, int32_t nb, int32_t k_coords,
+               const double *levels, int32_t n_fits, int32_t log_space, double *out_coeffs, int32_t *out_rank) {
+  if (!c || !design || !levels) return fail(BRM_EINVAL, "NULL argument");
+  if (c->hdr.rule != BRM_RULE_IZ) return fail(BRM_EINVAL, "context does not hold an I&Z boundary");
+  if (m < 1 || m >= c->hdr.n_dates) return fail(BRM_EINVAL, "boundary date %d outside 1..%d", m, c->hdr.n_dates - 1);
+  if (nb != c->hdr.nbasis) return fail(BRM_EINVAL, "basis size %d != the image's %d", nb, c->hdr.nbasis);
+  if (k_coords < 0 || nb != quad_basis_size(k_coords) || nb > kLsMaxB)
+    return fail(BRM_EINVAL, "basis size %d is not the quadratic basis of %d coordinates", nb, k_coords);
+  if (J < nb) return fail(BRM_EINVAL, "need at least %d probe points for the quadratic fit, got %d", nb, J);
+  if (J > kLsMaxN) return fail(BRM_EINVAL, "too many probe points for the device fit");
+  const int d = c->hdr.d;
+  const bool log_surface = c->hdr.iz_space == 1;
+  if (log_surface ? n_fits != 1 : n_fits != d)
+    return fail(BRM_EINVAL, "%d fits for a %s surface of d=%d", n_fits, log_surface ? "log-space" : "price", d);
+  if (ls_fit_smem(J, nb) > (size_t)c->info.max_smem) return fail(BRM_EINVAL, "design too large for the device fit");
+  DeviceScope scope(c->device);
+  Call call(c->stream());
+  BRM_CUDA(cudaStreamWaitEvent(call.stream, c->ready, 0));
+  LsParams P{};
+  BRM_TRY(call.in(design, (size_t)J * nb, &P.design));
+  BRM_TRY(call.in(levels, (size_t)J * n_fits, &P.levels));
+  BRM_TRY(call.out(out_coeffs, (size_t)n_fits * nb, &P.out));
+  BRM_TRY(call.out(out_rank, (size_t)n_fits, &P.rank_out));
+  P.J = J;
+  P.nb = nb;
+  P.k = k_coords;
+  P.log_space = log_space ? 1 : 0;
+  // the date's surface rows in the image: asset g's row, or (log space) every row
+  P.dst = reinterpret_cast<double *>(c->blob) + c->hdr.o_izc + (size_t)m * d * nb;
+  P.dst_fit_stride = nb;
+  P.dst_rows = log_surface ? d : 1;
+  BRM_TRY(launch_ls_fit(P, n_fits, call.stream));
+  BRM_CUDA(cudaEventRecord(c->ready, call.stream));  // later launches on any stream see the new surface
+  return call.finish();
+}
+
 int brm_ctx_destroy(brm_ctx *c) {
   if (!c) return BRM_OK;
   DeviceScope scope(c->device);
@@ -1166,13 +1229,42 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   cfg.blockDim = dim3(kWalkThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = call.stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = csize;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // Bisection tree: when the probes leave the GPU mostly idle (config 1: one
+  // probe per date), evaluate the 2^L - 1 midpoints of L bisection levels at
+  // once on as many clusters -- the same decisions and bits as L sequential
+  // passes (common random numbers), L times fewer passes.
+  P.tree_levels = 1;
+  P.tree_passes = 0;
+  P.tree_cont = nullptr;
+  if (solver == 1 && getenv("BRM_IZ_NO_TREE") == nullptr) {
+    const double span = (hi - lo) / tol;
+    int levels = span > 1.0 ? (int)std::ceil(std::log2(span)) + 2 : 2;
+    levels = std::min(levels, std::max(max_iter, 1));
+    int L = 1;
+    while (L < 6 && L < levels && n * (int64_t)((2 << L) - 1) * csize <= 2LL * c->info.sms) ++L;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    for (; L > 1; --L) {
+      cfg.gridDim = dim3((unsigned)(n * ((1 << L) - 1) * csize));
+      cfg.numAttrs = 2;
+      if ((int64_t)max_active_clusters(kiz, cfg, c->device) >= n * ((1 << L) - 1)) break;
+    }
+    if (L > 1) {
+      P.tree_levels = L;
+      P.tree_passes = (levels + L - 1) / L;
+      BRM_TRY(call.scratch((size_t)2 * n * ((1 << L) - 1), &P.tree_cont));
+    } else {
+      cfg.gridDim = dim3((unsigned)(n * csize));
+      cfg.numAttrs = 1;
+    }
+  }
   void *args[] = {&P};
   {
     const int tok_ = prof_begin(PK_IZ, call.stream);

@@ -76,6 +76,10 @@ struct IzParams {
   unsigned long long *steps;
   double *out_level;
   int32_t *out_iter, *out_conv;
+  // bisection tree (solver 1): tree_levels > 1 evaluates 2^L - 1 midpoints
+  // per pass on as many clusters (cooperative launch), tree_passes passes
+  int tree_levels, tree_passes;
+  double *tree_cont;  // [2][n_probes][2^L - 1] node continuation values
 };
 
 struct DecisionParams {
@@ -132,6 +136,22 @@ struct SlotDims {
 inline SlotDims slot_dims(int capacity, int nfeat) { return SlotDims{std::max(2 * capacity, 1), capacity + nfeat}; }
 constexpr int kMaxSlotStumps = 1024;
 void *set_ensemble_kernel();
+
+// Device quadratic regression (brm_boost.cu): n_fits fits of design [J][nb]
+// against levels [n_fits][J], coefficients optionally written into a rule image.
+struct LsParams {
+  const double *design;  // [J][nb] row-major
+  const double *levels;  // [n_fits][J]
+  int J, nb, k, log_space;
+  double *out;           // [n_fits][nb] (may be null)
+  int *rank_out;         // [n_fits] (may be null)
+  double *dst;           // rule-image surface of the date (may be null)
+  int dst_fit_stride;    // doubles between fits' first rows in dst
+  int dst_rows;          // rows written per fit (nb doubles apart)
+};
+constexpr int kLsMaxN = 4096, kLsMaxB = 64;
+int launch_ls_fit(const LsParams &P, int n_fits, cudaStream_t s);
+size_t ls_fit_smem(int J, int nb);
 size_t set_ensemble_smem(int capacity);
 
 // Keep freed stream-ordered allocations in the device's default pool across

@@ -133,7 +133,10 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int csize = (int)cluster.num_blocks();
-  const int probe = blockIdx.x / csize;
+  // tree mode: clusters (probe, node slot) of the bisection tree; else one cluster per probe
+  const int n_slots = P.tree_levels > 1 ? (1 << P.tree_levels) - 1 : 1;
+  const int probe = (int)(blockIdx.x / csize) / n_slots;
+  const int probe_slot = (int)(blockIdx.x / csize) % n_slots;
 
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_next;
@@ -178,6 +181,100 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
   cluster.sync();
   double *x_remote = cluster.map_shared_rank(&s_x, 0);
   int *done_remote = cluster.map_shared_rank(&s_done, 0);
+
+  if (P.tree_levels > 1) {
+    // ---- bisection tree (solver 1, cooperative launch) --------------------
+    // Cluster (probe, slot) evaluates node `slot` of a complete binary tree
+    // of tree_levels bisection levels below the probe's current bracket,
+    // every node with the same draws (common random numbers, draw_base 0).
+    // After a grid barrier every cluster of the probe walks the tree with
+    // the nodes' continuation values and takes the bracket binary bisection
+    // would reach after those levels: the same midpoints (the same fp64
+    // operations), decisions, iteration count and bits, in 1 / tree_levels
+    // of the sequential passes.
+    cg::grid_group grid = cg::this_grid();
+    const int kt = (1 << P.tree_levels) - 1;
+    const int slot = probe_slot;
+    for (int pass = 0; pass < P.tree_passes; ++pass) {
+      if (rank == 0 && threadIdx.x == 0 && !s_done) {
+        // the slot's midpoint: descend from the bracket along the heap path
+        double l = s_lo, h = s_hi;
+        const int path = slot + 1;
+        const int depth = 31 - __clz(path);
+        for (int t = depth - 1; t >= 0; --t) {
+          const double xm = __dmul_rn(0.5, __dadd_rn(l, h));
+          if ((path >> t) & 1) l = xm;
+          else h = xm;
+        }
+        s_x = __dmul_rn(0.5, __dadd_rn(l, h));
+      }
+      cluster.sync();
+      const bool done = *done_remote != 0;
+      if (!done) {
+        const double x = *x_remote;
+        if (threadIdx.x == 0) probe_state(P.hdr, seedp, asset, x, s_state);
+        __syncthreads();
+        if (threadIdx.x < d) s_start[threadIdx.x] = (R)s_state[threadIdx.x];
+        if (threadIdx.x == 0) s_next = p0 + blockDim.x;
+        __syncthreads();
+        const uint64_t base0 = unit_base<FAST>(0, P.normals != nullptr);
+        if (p0 < p1)
+          walk_paths<D, FAST, GEOK ? WALK_GEO : WALK_GENERIC>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1,
+                                                              ns, vals, &s_next, nullptr, nullptr, P.steps, tq);
+        __syncthreads();
+        fold_chunks(vals, p1 > p0 ? p1 - p0 : 0, s_chunk);
+      }
+      cluster.sync();
+      double *cont_buf = P.tree_cont + (size_t)(pass & 1) * P.n_probes * kt + (size_t)probe * kt;
+      if (rank == 0 && threadIdx.x == 0 && !done) {
+        double total = 0.0;
+        for (int r = 0; r < csize; ++r) {
+          const double *rc = cluster.map_shared_rank(s_chunk, r);
+          for (int c = 0; r * per_cta + c * kIzFoldChunk < min((r + 1) * per_cta, P.n_inner); ++c)
+            total = __dadd_rn(total, rc[c]);
+        }
+        cont_buf[slot] = __ddiv_rn(total, (double)P.n_inner);
+      }
+      grid.sync();  // (double-buffered by pass: a cluster may publish pass p+1 while another reads pass p)
+      if (rank == 0 && threadIdx.x == 0 && !s_done) {
+        double l = s_lo, h = s_hi;
+        int j = 0, n_it = s_it;
+        bool fin = false;
+        for (int t = 0; t < P.tree_levels && !fin; ++t) {
+          const double xm = __dmul_rn(0.5, __dadd_rn(l, h));
+          double st[kMaxD];
+          probe_state(P.hdr, seedp, asset, xm, st);
+          Model<double> Md{};
+          Md.d = d;
+          Md.payoff = P.hdr.payoff;
+          Md.strike = K;
+          const double pay = payoff<0>(Md, st);
+          const bool exercise = __dsub_rn(pay, __ldcg(cont_buf + j)) > 0.0;
+          if (call_like == exercise) {
+            h = xm;
+            j = 2 * j + 1;
+          } else {
+            l = xm;
+            j = 2 * j + 2;
+          }
+          ++n_it;
+          fin = !(__dsub_rn(h, l) > P.tol) || n_it >= P.max_iter;
+        }
+        s_lo = l;
+        s_hi = h;
+        s_it = n_it;
+        s_done = fin ? 1 : 0;
+      }
+    }
+    if (rank == 0 && threadIdx.x == 0 && slot == 0) {
+      double st[kMaxD];
+      P.out_level[probe] = probe_state(P.hdr, seedp, asset, __dmul_rn(0.5, __dadd_rn(s_lo, s_hi)), st);
+      P.out_iter[probe] = s_it;
+      P.out_conv[probe] = !(__dsub_rn(s_hi, s_lo) > P.tol);
+    }
+    cluster.sync();
+    return;
+  }
 
   for (int it = 0;; ++it) {
     if (*done_remote) break;

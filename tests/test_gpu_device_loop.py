@@ -124,3 +124,56 @@ def test_set_ensemble_rejects_bad_calls():
         slot.set_ensemble(int(mp.n_dates), np.zeros(4, np.int32), z, z, z, np.array([0], np.int32), np.array([1.0]))
     with pytest.raises(ValueError):
         Context.cmc_slots(mp, True, 0, mode="parity")
+
+
+IZ_CASES = [
+    # (d, payoff, J, n_inner, solver, kwargs): C1-like put, d=3 max-call, C2-like geometric put
+    (1, "put", 1, 2000, "bisection", dict(bracket=(20.0, 40.0), tol=1e-4)),
+    (1, "put", 4, 500, "fixed_point", dict(max_iter=40)),
+    (3, "maxcall", 16, 300, "fixed_point", dict(max_iter=30)),
+    (5, "geoput", 32, 400, "bisection", dict(bracket=(50.0, 100.0), tol=1e-3)),
+]
+
+
+def _iz_objects(d, payoff):
+    if payoff == "put":
+        return E.MarketParams(d=1, s0=40.0, r=0.06, sigma=0.2), E.BermudanSpec(40.0, 1.0, 10, E.PayoffKind.PUT_1D)
+    if payoff == "geoput":
+        return (E.MarketParams(d=d, s0=100.0, r=0.03, sigma=0.4),
+                E.BermudanSpec(100.0, 1.0, 10, E.PayoffKind.GEO_PUT))
+    return E.MarketParams(d=d, s0=100.0, r=0.05, sigma=0.2, delta=0.1), E.BermudanSpec(100.0, 3.0, 9)
+
+
+@pytest.mark.parametrize("case", IZ_CASES, ids=lambda c: f"{c[1]}-d{c[0]}-{c[4]}")
+def test_iz_device_loop_equals_host_loop(case):
+    """The device-resident I&Z date loop (levels, exchange and regression in HBM,
+    surfaces written into the rule image by brm_iz_fit) reproduces the
+    host-driven loop bit for bit: levels, iteration counts, coefficients, price."""
+    d, payoff, J, n_inner, solver, kw = case
+    params, spec = _iz_objects(d, payoff)
+    a, ra = E.build_iz_boundary(params, spec, J, n_inner, seed=11, solver=solver, mode="parity", device_loop=True, **kw)
+    b, rb = E.build_iz_boundary(params, spec, J, n_inner, seed=11, solver=solver, mode="parity", device_loop=False,
+                                **kw)
+    assert ra.iteration_counts == rb.iteration_counts
+    assert ra.unconverged_points == rb.unconverged_points
+    assert np.array_equal(a.coeffs, b.coeffs)
+    pa = E.price(params, spec, E.IzRule(a), 1 << 14, 3, mode="parity")
+    pb = E.price(params, spec, E.IzRule(b), 1 << 14, 3, mode="parity")
+    assert pa.price == pb.price
+
+
+def test_bisection_tree_equals_sequential_bisection(monkeypatch):
+    """The bisection tree (2^L - 1 midpoints per pass on as many clusters)
+    takes exactly the sequential bisection's decisions: same levels, iteration
+    counts and convergence flags, for one probe (C1: the tree is used) and for
+    many (the tree is off when the probes fill the GPU)."""
+    for d, payoff, J, n_inner, kw in [(1, "put", 1, 2000, dict(bracket=(20.0, 40.0), tol=1e-4)),
+                                      (1, "put", 3, 700, dict(bracket=(20.0, 40.0), tol=1e-6)),
+                                      (5, "geoput", 24, 300, dict(bracket=(50.0, 100.0), tol=1e-4))]:
+        params, spec = _iz_objects(d, payoff)
+        monkeypatch.delenv("BRM_IZ_NO_TREE", raising=False)
+        a, ra = E.build_iz_boundary(params, spec, J, n_inner, seed=5, solver="bisection", mode="parity", **kw)
+        monkeypatch.setenv("BRM_IZ_NO_TREE", "1")
+        b, rb = E.build_iz_boundary(params, spec, J, n_inner, seed=5, solver="bisection", mode="parity", **kw)
+        assert ra.iteration_counts == rb.iteration_counts
+        assert np.array_equal(a.coeffs, b.coeffs), payoff
