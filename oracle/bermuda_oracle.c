@@ -514,3 +514,140 @@ ORC_API int orc_sample_points(const orc_ctx *c, int mode, int m, int64_t n, cons
     }
     return 0;
 }
+
+/* ----------------------------------------------- batched (threads) ----- */
+/* The restated CPU pricer (oracle/restated.py) for the configs the reference
+ * cannot express: independent items spread over the host cores (POSIX
+ * threads, a shared atomic item counter), one stream per item as in the
+ * engine.  ORC_THREADS overrides the thread count (default: online cores). */
+#include <pthread.h>
+#include <stdatomic.h>
+#include <unistd.h>
+
+typedef struct {
+    atomic_long next;
+    int64_t n;
+    void (*fn)(void *arg, int64_t i);
+    void *arg;
+} orc_pool;
+
+static void *orc_worker(void *p) {
+    orc_pool *pool = (orc_pool *)p;
+    for (;;) {
+        int64_t i = atomic_fetch_add(&pool->next, 1);
+        if (i >= pool->n) break;
+        pool->fn(pool->arg, i);
+    }
+    return NULL;
+}
+
+ORC_API int orc_threads(void) {
+    const char *e = getenv("ORC_THREADS");
+    long t = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+    return t < 1 ? 1 : (t > 512 ? 512 : (int)t);
+}
+
+static void orc_parallel_for(int64_t n, void (*fn)(void *, int64_t), void *arg) {
+    orc_pool pool;
+    atomic_init(&pool.next, 0);
+    pool.n = n;
+    pool.fn = fn;
+    pool.arg = arg;
+    int nt = orc_threads();
+    if (nt > n) nt = (int)n;
+    pthread_t th[512];
+    int started = 0;
+    for (int t = 1; t < nt; ++t)
+        if (pthread_create(&th[started], NULL, orc_worker, &pool) == 0) ++started;
+    orc_worker(&pool);
+    for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+}
+
+typedef struct {
+    const orc_ctx *c;
+    const double *points;
+    int m, n_label;
+    const uint64_t *keys, *streams;
+    uint64_t draw_base;
+    double *out;
+} orc_labels_job;
+
+static void orc_labels_item(void *p, int64_t i) {
+    const orc_labels_job *j = (const orc_labels_job *)p;
+    orc_cmc_labels(j->c, j->points + i * j->c->d, 1, j->m, j->n_label, j->keys + i, j->streams + i, j->draw_base,
+                   j->out + i);
+}
+
+/* orc_cmc_labels over the host cores. */
+ORC_API int orc_cmc_labels_mt(const orc_ctx *c, const double *points, int64_t n, int m, int n_label,
+                              const uint64_t *keys, const uint64_t *streams, uint64_t draw_base, double *out) {
+    if (c->n_dates - m <= 0) return -1;
+    orc_labels_job j = {c, points, m, n_label, keys, streams, draw_base, out};
+    orc_parallel_for(n, orc_labels_item, &j);
+    return 0;
+}
+
+typedef struct {
+    const orc_ctx *c;
+    const double *seeds;
+    int seed_stride;
+    const int32_t *assets;
+    int m, n_inner, max_iter;
+    double lo, hi, tol;
+    uint64_t seed;
+    int64_t item_lo;
+    double *level;
+    int32_t *iterations, *converged;
+} orc_bisect_job;
+
+static void orc_bisect_item(void *p, int64_t i) {
+    const orc_bisect_job *j = (const orc_bisect_job *)p;
+    uint64_t key, stream;
+    orc_derive_words(j->seed, 1, (uint64_t)(j->item_lo + i), (uint64_t)j->m, &key, &stream);
+    double zero = 0.0;
+    orc_iz_bisect(j->c, j->seed_stride ? j->seeds + i * j->seed_stride : &zero, j->assets[i], j->m, j->n_inner, j->lo,
+                  j->hi, j->tol, j->max_iter, key, stream, j->level + i, j->iterations + i, j->converged + i);
+}
+
+/* n bisection solves (orc_iz_bisect) on streams derive(seed, IZ_CALC, item_lo + j, m), over the host cores. */
+ORC_API int orc_iz_bisect_batch(const orc_ctx *c, const double *seeds, int seed_stride, const int32_t *assets,
+                                int64_t n, int m, int n_inner, double lo, double hi, double tol, int max_iter,
+                                uint64_t seed, int64_t item_lo, double *level, int32_t *iterations,
+                                int32_t *converged) {
+    if (c->n_dates - m <= 0) return -1;
+    orc_bisect_job j = {c, seeds, seed_stride, assets, m, n_inner, max_iter, lo, hi, tol, seed, item_lo, level,
+                        iterations, converged};
+    orc_parallel_for(n, orc_bisect_item, &j);
+    return 0;
+}
+
+typedef struct {
+    const orc_ctx *c;
+    const double *s0;
+    int64_t n_paths, block_lo;
+    uint64_t seed;
+    double *out;
+} orc_price_job;
+
+static void orc_price_item(void *p, int64_t i) {
+    const orc_price_job *j = (const orc_price_job *)p;
+    const int64_t b = j->block_lo + i;
+    int64_t cnt = j->n_paths - b * 4096;
+    if (cnt > 4096) cnt = 4096;
+    uint64_t key, stream;
+    orc_derive_words(j->seed, 3, (uint64_t)b, 0, &key, &stream);
+    double s, q;
+    orc_stopped_sums(j->c, j->s0, 0, cnt, key, stream, 0, &s, &q);
+    j->out[3 * i] = (double)cnt;
+    j->out[3 * i + 1] = s;
+    j->out[3 * i + 2] = q;
+}
+
+/* Per-block (count, sum, sumsq) of 4096-path pricing blocks [block_lo, block_hi)
+ * (pricer.py:154-164) on streams derive(seed, PRICING, b, 0), over the host cores. */
+ORC_API int orc_price_blocks(const orc_ctx *c, const double *s0, int64_t n_paths, uint64_t seed, int64_t block_lo,
+                             int64_t block_hi, double *out) {
+    orc_price_job j = {c, s0, n_paths, block_lo, seed, out};
+    orc_parallel_for(block_hi - block_lo, orc_price_item, &j);
+    return 0;
+}

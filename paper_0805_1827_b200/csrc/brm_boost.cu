@@ -950,6 +950,10 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       int sms = 148;
       BCU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
       int cl = std::max(1, std::min(kCbMaxCluster, sms / F));
+      // BRM_NCU_SAFE: one CTA per feature, no cluster launch attribute (Nsight
+      // Compute cannot replay cooperative cluster launches); same results
+      const bool ncu_safe = getenv("BRM_NCU_SAFE") != nullptr;
+      if (ncu_safe) cl = 1;
       const int L = (int)tree.leaves.size();
       // (slice_cap, pos_cap, dynamic shared memory) for cluster size c
       auto layout = [&](int c, int &slice_cap, int &pos_cap) {
@@ -997,6 +1001,10 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
         at[1].val.clusterDim.x = cl;
         lc.gridDim = dim3((unsigned)(F * cl));
         lc.dynamicSmemBytes = dyn;
+        if (ncu_safe) {
+          lc.numAttrs = 1;
+          break;
+        }
         int max_clusters = 0;
         if (cudaOccupancyMaxActiveClusters(&max_clusters, (void *)boost_cluster_kernel, &lc) != cudaSuccess) {
           cudaGetLastError();

@@ -1243,7 +1243,8 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   P.tree_levels = 1;
   P.tree_passes = 0;
   P.tree_cont = nullptr;
-  if (solver == 1 && getenv("BRM_IZ_NO_TREE") == nullptr) {
+  // (BRM_NCU_SAFE: Nsight Compute cannot replay cooperative cluster launches)
+  if (solver == 1 && getenv("BRM_IZ_NO_TREE") == nullptr && getenv("BRM_NCU_SAFE") == nullptr) {
     const double span = (hi - lo) / tol;
     int levels = span > 1.0 ? (int)std::ceil(std::log2(span)) + 2 : 2;
     levels = std::min(levels, std::max(max_iter, 1));

@@ -177,3 +177,26 @@ def test_bisection_tree_equals_sequential_bisection(monkeypatch):
         b, rb = E.build_iz_boundary(params, spec, J, n_inner, seed=5, solver="bisection", mode="parity", **kw)
         assert ra.iteration_counts == rb.iteration_counts
         assert np.array_equal(a.coeffs, b.coeffs), payoff
+
+
+def test_partitions_give_identical_bits_at_c2_probe_count():
+    """Any item partition (1, 2, 3, 8 GPUs' worth, dist.virtual_shards) gives the
+    same boundary and price bits at C2's full probe count (64 probes, 5000
+    inner paths): the probe clusters fold their paths in fixed 256-path
+    chunks, so the continuation value does not depend on how many probes
+    share a launch (cluster size) -- and the bisection tree's decisions equal
+    the sequential ones."""
+    from paper_0805_1827_b200.dist import virtual_shards
+    params = E.MarketParams(d=5, s0=100.0, r=0.03, sigma=0.4)
+    spec = E.BermudanSpec(100.0, 1.0, 10, E.PayoffKind.GEO_PUT)
+    out = []
+    for parts in (1, 2, 3, 8):
+        with virtual_shards(parts):
+            b, rep = E.build_iz_boundary(params, spec, 64, 5000, seed=1827, solver="bisection",
+                                         bracket=(50.0, 100.0), tol=1e-4, mode="parity")
+            est = E.price(params, spec, E.IzRule(b), 1 << 16, 1827, mode="parity")
+        out.append((b.coeffs, rep.iteration_counts, est.price))
+    for coeffs, its, p in out[1:]:
+        assert np.array_equal(coeffs, out[0][0])
+        assert its == out[0][1]
+        assert p == out[0][2]
