@@ -18,8 +18,11 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIBDIR = PKG / "lib"
-LIB = LIBDIR / "libbermuda_b200.so"
-OBJDIR = PKG / "lib" / "obj"
+# BRM_LIB_OUT / BRM_NVCC_DEFS: build a variant library elsewhere (A/B timing of
+# compile-time kernel options, loaded with BRM_LIB_PATH)
+LIB = Path(os.environ["BRM_LIB_OUT"]) if os.environ.get("BRM_LIB_OUT") else LIBDIR / "libbermuda_b200.so"
+OBJDIR = LIB.parent / "obj"
+EXTRA_DEFS = os.environ.get("BRM_NVCC_DEFS", "").split()
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -43,7 +46,7 @@ def _stale() -> bool:
 
 def _compile(src: Path, ptxas_v: bool) -> tuple[Path, str]:
     obj = OBJDIR / (src.stem + ".o")
-    cmd = [_nvcc(), *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [_nvcc(), *ARCH, *FLAGS, *EXTRA_DEFS, "-c", str(src), "-o", str(obj)]
     if ptxas_v:
         cmd += ["-Xptxas", "-v"]
     res = subprocess.run(cmd, capture_output=True, text=True)
