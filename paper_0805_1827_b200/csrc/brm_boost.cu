@@ -39,7 +39,6 @@ namespace cg = cooperative_groups;
 
 namespace brm {
 
-constexpr int kBoostThreads = 256;
 constexpr int kPwBlock = 128;  // numpy PW_BLOCKSIZE
 
 // numpy pairwise_sum leaf (n <= 128): 8 strided accumulators, fixed combine,
@@ -287,232 +286,6 @@ void *exact_scan_selftest_kernel() { return (void *)&exact_scan_selftest; }
 }  // namespace brm
 #include "brm_boost_cluster.cuh"
 namespace brm {
-
-// ---------------------------------------------------------- fast mode ----
-// BRM_MODE_FAST AdaBoost: the same stump search and boosting rules, with the
-// weights quantised to 62-bit fixed point for the split search.  Integer
-// prefix sums are exact and associative, so every prefix is a parallel block
-// scan (no sequential fp64 chain) and the result is identical for any
-// scheduling; the fp64 weights are renormalised in a fixed tree order.
-// Statistically equivalent to the reference, not bit-identical to numpy.
-constexpr double kFix = 4611686018427387904.0;  // 2^62
-
-struct FastBoostParams {
-  int n, F, rounds, raw;
-  const double *xs, *xsorted, *y;
-  const int *order;
-  double *ysorted;              // [F][n] labels in each feature's sorted order (filled by the kernel)
-  double *wpart;                // [gridDim] per-slice sums of the new weights (fixed CTA order)
-  double *w;                    // [n] fp64 weights (unnormalised between rounds)
-  long long *feat_err;          // [F] best integer error of each feature
-  int *feat_pos;                // [F]
-  int *out_feat;
-  double *out_thr, *out_pol, *out_alpha, *out_err;
-  int *out_count;
-  double *out_intercept;
-  const int *n_pos;  // positives in the training set (device)
-};
-
-// Fixed-order CTA sum (thread-strided runs, shuffle tree, warps in order).
-__device__ double cta_sum_fixed(const double *a, int n, double *s_red) {
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += a[i];
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < (int)blockDim.x / 32; ++w) t += s_red[w];
-  __syncthreads();
-  return t;
-}
-
-__device__ __forceinline__ long long fixw(double w, double inv_s) { return __double2ll_rn(w * inv_s * kFix); }
-
-__global__ void __launch_bounds__(kBoostThreads) boost_fast_kernel(FastBoostParams P) {
-  using Scan = cub::BlockScan<long long, kBoostThreads>;
-  __shared__ typename Scan::TempStorage s_scan;
-  __shared__ double s_red[kBoostThreads / 32];
-  __shared__ long long s_carry_p, s_carry_n;
-  __shared__ struct { long long err; int key; } s_cand[kBoostThreads / 32];
-  __shared__ int s_stop, s_feat;
-  __shared__ double s_thr, s_pol, s_alpha, s_err;
-  cg::grid_group grid = cg::this_grid();
-  const int n = P.n, F = P.F, f = blockIdx.x;
-  const int slice = (n + gridDim.x - 1) / gridDim.x;
-  const int w_lo = blockIdx.x * slice, w_hi = min(w_lo + slice, n);
-  const int n_pos_all = *P.n_pos;
-  if (one_class_exit(P.raw, n, n_pos_all, P.out_count, P.out_intercept)) return;
-  int count = 0;
-  const int *ord = P.order + (size_t)f * n;
-  const double *xf = P.xsorted + (size_t)f * n;
-  double *ysf = P.ysorted + (size_t)f * n;
-  // labels in this feature's sorted order, once per fit: the split scan then
-  // gathers only the weights
-  for (int i = threadIdx.x; i < n; i += blockDim.x) ysf[i] = P.y[ord[i]];
-  __syncthreads();
-  for (int round = 0; round < P.rounds; ++round) {
-    // sum of the weights: round 0 by every CTA, later rounds from the slice
-    // sums the previous reweight published (same order in every CTA)
-    double ssum;
-    if (round == 0) {
-      ssum = cta_sum_fixed(P.w, n, s_red);
-    } else {
-      if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(P.wpart + b);
-        s_red[0] = t;
-      }
-      __syncthreads();
-      ssum = s_red[0];
-      __syncthreads();
-    }
-    const double inv_s = 1.0 / ssum;
-    if (threadIdx.x == 0) s_carry_p = s_carry_n = 0;
-    __syncthreads();
-    // split search: one block scan per tile of sorted positions.  With d_i =
-    // (positives - negatives up to i), err+ = d_i + tot_neg and err- = tot_pos
-    // - d_i, so the argmins need only min / max of d_i; the class totals are
-    // the scan's final carries
-    long long dmin = LLONG_MAX, dmax = LLONG_MIN;
-    int kmin = INT_MAX, kmax = INT_MAX;
-    constexpr int ITEMS = 8;  // consecutive sorted positions per thread per tile
-    for (int t0 = 0; t0 < n; t0 += ITEMS * blockDim.x) {
-      const int i0 = t0 + threadIdx.x * ITEMS;
-      long long wp[ITEMS], wn_[ITEMS];
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k) {
-        const int i = i0 + k;
-        wp[k] = wn_[k] = 0;
-        if (i < n) {
-          const long long W = fixw(P.w[ord[i]], inv_s);
-          if (ysf[i] > 0.0) wp[k] = W;
-          else wn_[k] = W;
-        }
-      }
-      long long lp = 0, ln = 0;
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k) lp += wp[k], ln += wn_[k];
-      long long ep_, en_, sp, sn;
-      Scan(s_scan).ExclusiveSum(lp, ep_, sp);
-      __syncthreads();
-      Scan(s_scan).ExclusiveSum(ln, en_, sn);
-      long long cp = s_carry_p + ep_, cn = s_carry_n + en_;
-#pragma unroll
-      for (int k = 0; k < ITEMS; ++k) {
-        const int i = i0 + k;
-        cp += wp[k];
-        cn += wn_[k];
-        if (i < n - 1 && __dsub_rn(xf[i + 1], xf[i]) > 0.0) {
-          const long long dd = cp - cn;
-          if (dd < dmin) dmin = dd, kmin = 2 * i;        // positions ascend: first hit keeps the lowest key
-          if (dd > dmax) dmax = dd, kmax = 2 * i + 1;
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        s_carry_p += sp;
-        s_carry_n += sn;
-      }
-      __syncthreads();
-    }
-    const long long tot_pos = s_carry_p, tot_neg = s_carry_n, total = tot_pos + tot_neg;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const long long o1 = __shfl_down_sync(0xffffffffu, dmin, off), o2 = __shfl_down_sync(0xffffffffu, dmax, off);
-      const int k1 = __shfl_down_sync(0xffffffffu, kmin, off), k2 = __shfl_down_sync(0xffffffffu, kmax, off);
-      if (o1 < dmin || (o1 == dmin && k1 < kmin)) dmin = o1, kmin = k1;
-      if (o2 > dmax || (o2 == dmax && k2 < kmax)) dmax = o2, kmax = k2;
-    }
-    if ((threadIdx.x & 31) == 0) {
-      // this warp's best of the two error lists (lowest key at equal error)
-      long long best_err = LLONG_MAX;
-      int best_key = INT_MAX;
-      if (kmin != INT_MAX) best_err = dmin + tot_neg, best_key = kmin;
-      if (kmax != INT_MAX) {
-        const long long em = tot_pos - dmax;
-        if (em < best_err || (em == best_err && kmax < best_key)) best_err = em, best_key = kmax;
-      }
-      s_cand[threadIdx.x >> 5] = {best_err, best_key};
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long best_err = s_cand[0].err;
-      int best_key = s_cand[0].key;
-      for (int w = 1; w < (int)blockDim.x / 32; ++w)
-        if (s_cand[w].err < best_err || (s_cand[w].err == best_err && s_cand[w].key < best_key))
-          best_err = s_cand[w].err, best_key = s_cand[w].key;
-      P.feat_err[f] = best_err;
-      P.feat_pos[f] = best_key;
-    }
-    grid.sync();
-    if (threadIdx.x == 0) {
-      long long be = LLONG_MAX;
-      int bf = -1, bk = 0;
-      for (int g = 0; g < F; ++g)
-        if (P.feat_pos[g] != INT_MAX && P.feat_err[g] < be) be = P.feat_err[g], bf = g, bk = P.feat_pos[g];
-      if (bf < 0) {  // every feature constant: majority constant stump
-        const double pol = 2 * tot_neg <= total ? 1.0 : -1.0;  // +1 iff sum(w y) >= 0
-        s_feat = 0;
-        s_thr = __longlong_as_double(0xfff0000000000000LL);
-        s_pol = pol;
-        s_err = (double)(pol > 0 ? tot_neg : total - tot_neg) / (double)total;
-      } else {
-        const double *xb = P.xsorted + (size_t)bf * n;
-        const int i = bk >> 1;
-        s_feat = bf;
-        s_thr = 0.5 * (xb[i] + xb[i + 1]);
-        s_pol = (bk & 1) ? -1.0 : 1.0;
-        s_err = (double)be / (double)total;
-      }
-      const double err = s_err;
-      if (P.raw) {
-        if (blockIdx.x == 0) {
-          P.out_feat[0] = s_feat, P.out_thr[0] = s_thr, P.out_pol[0] = s_pol, P.out_alpha[0] = 1.0;
-          P.out_err[0] = err;
-        }
-        s_stop = 3;
-      } else if (err >= 0.5) {
-        s_stop = 1;
-      } else {
-        const double a = 0.5 * log((1.0 - err) / (err > 1e-10 ? err : 1e-10));
-        s_alpha = a;
-        if (blockIdx.x == 0) {
-          P.out_feat[count] = s_feat, P.out_thr[count] = s_thr, P.out_pol[count] = s_pol;
-          P.out_alpha[count] = a, P.out_err[count] = err;
-        }
-        s_stop = err <= 0.0 ? 3 : 0;
-      }
-    }
-    __syncthreads();
-    if (s_stop == 1) break;
-    ++count;
-    if (s_stop == 3 || round + 1 == P.rounds) break;
-    {
-      const double a = s_alpha, thr = s_thr, pol = s_pol;
-      const int feat = s_feat;
-      const double e_agree = exp(-a), e_miss = exp(a);
-      double part = 0.0;
-      for (int i = w_lo + threadIdx.x; i < w_hi; i += blockDim.x) {
-        const double pred = P.xs[(size_t)i * F + feat] > thr ? pol : -pol;
-        const double wn = P.w[i] * inv_s * ((P.y[i] * pred > 0.0) ? e_agree : e_miss);
-        P.w[i] = wn;
-        part += wn;
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) part += __shfl_down_sync(0xffffffffu, part, off);
-      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = part;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < (int)blockDim.x / 32; ++w) t += s_red[w];
-        P.wpart[blockIdx.x] = t;
-      }
-    }
-    grid.sync();
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) write_result(count, n, n_pos_all, P.out_count, P.out_intercept);
-}
 
 __global__ void transpose_cols(const double *xs, int n, int F, double *xt, int *iota) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -857,36 +630,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       d_count = out_count;
       d_icept = out_intercept;
     }
-    if (mode == BRM_MODE_FAST) {
-      FastBoostParams Q{};
-      Q.n = n;
-      Q.F = F;
-      Q.rounds = rounds;
-      Q.raw = raw ? 1 : 0;
-      Q.xs = d_xs;
-      Q.xsorted = d_xsorted;
-      Q.y = d_y;
-      Q.order = d_order;
-      Q.w = d_w;
-      BCU(S.get(&Q.ysorted, (size_t)F * n));
-      BCU(S.get(&Q.wpart, F));
-      long long *d_ferr = nullptr;
-      BCU(S.get(&d_ferr, F));
-      Q.feat_err = d_ferr;
-      Q.feat_pos = d_pos;
-      Q.out_feat = d_feat;
-      Q.out_thr = d_thr;
-      Q.out_pol = d_pol;
-      Q.out_alpha = d_alpha;
-      Q.out_err = d_rerr;
-      Q.out_count = d_count;
-      Q.out_intercept = d_icept;
-      Q.n_pos = d_npos;
-      void *qargs[] = {&Q};
-      const int tok = prof_begin(PK_BOOST, s);
-      BCU(cudaLaunchCooperativeKernel((void *)boost_fast_kernel, dim3(F), dim3(kBoostThreads), qargs, 0, s));
-      prof_end(tok, s);
-    } else {
+    {
       BCU(S.get(&d_code, (size_t)n * F));
       {
         const int tok = prof_begin(PK_AUX, s);
@@ -980,7 +724,8 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
         rc = bfail(BRM_EINVAL, "training set too large for the device AdaBoost's shared memory");
         goto done;
       }
-      BCU(cudaFuncSetAttribute((void *)boost_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+      void *kfn = mode == BRM_MODE_FAST ? (void *)boost_fast_cluster_kernel : (void *)boost_cluster_kernel;
+      BCU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
       cudaLaunchConfig_t lc{};
       cudaLaunchAttribute at[2];
       lc.blockDim = dim3(kCbThreads);
@@ -996,8 +741,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       // every cluster must be resident at once (grid barrier)
       for (;; --cl) {
         dyn = layout(cl, slice_cap, pos_cap);
-        BCU(cudaFuncSetAttribute((void *)boost_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)dyn));
+        BCU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
         at[1].val.clusterDim.x = cl;
         lc.gridDim = dim3((unsigned)(F * cl));
         lc.dynamicSmemBytes = dyn;
@@ -1006,7 +750,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
           break;
         }
         int max_clusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&max_clusters, (void *)boost_cluster_kernel, &lc) != cudaSuccess) {
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, kfn, &lc) != cudaSuccess) {
           cudaGetLastError();
           max_clusters = 0;
         }
@@ -1019,12 +763,15 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       double *d_fthr;
       BCU(S.get(&d_fthr, 2 * F));
       P.feat_thr = d_fthr;
+      BCU(S.get(&P.feat_ierr, 2 * F));
       BCU(S.get(&P.chain_g, (size_t)2 * n * F));
       BCU(S.get(&P.wsub, (size_t)n * F * cl));
       {
         void *args[] = {&P};
         const int tok = prof_begin(PK_BOOST, s);
-        BCU(cudaLaunchKernelExC(&lc, (void *)boost_cluster_kernel, args));
+        // fast mode: the same cluster layout with fixed-point integer scans
+        BCU(cudaLaunchKernelExC(&lc, mode == BRM_MODE_FAST ? (void *)boost_fast_cluster_kernel
+                                                            : (void *)boost_cluster_kernel, args));
         prof_end(tok, s);
       }
       if (timing) {

@@ -55,6 +55,7 @@ struct CbParams {
   double *feat_err;        // [2][F]
   int *feat_pos;           // [2][F]
   double *feat_thr;        // [2][F] the candidate's threshold (boosting.py:148)
+  long long *feat_ierr;    // [2][F] fast mode: the candidate's fixed-point error
   int *out_feat;
   double *out_thr, *out_pol, *out_alpha, *out_err;
   int *out_count;
@@ -722,6 +723,253 @@ __global__ void __launch_bounds__(kCbThreads, 1) boost_cluster_kernel(CbParams P
 inline size_t cb_smem_bytes(int L, int n_children, int n_levels, int slice_cap, int pos_cap) {
   const size_t head = sizeof(double) * (4 * (size_t)L + slice_cap) + sizeof(unsigned) * pos_cap + slice_cap;
   return ((head + 15) & ~(size_t)15) + sizeof(int2) * (L + n_children) + sizeof(int) * n_levels;
+}
+
+// ------------------------------------------------------------- fast mode ----
+// BRM_MODE_FAST AdaBoost on the same cluster layout: the split search scans
+// weights quantised to 62-bit fixed point (W_i = rint(w_i / s 2^62)), so every
+// prefix is an exact integer scan -- no events, no walker -- and the result
+// is identical for any schedule.  The weight sum s is numpy's pairwise order
+// over the leaves (every CTA combines the same leaf sums), so it does not
+// depend on the cluster size.  Statistically equivalent to the reference,
+// not bit-identical to numpy (tests/test_gpu_config_parity.py, fast mode).
+constexpr double kFixC = 4611686018427387904.0;  // 2^62
+
+struct CbFastCand {
+  long long dmin, dmax;
+  int kmin, kmax;
+};
+
+__global__ void __launch_bounds__(kCbThreads, 1) boost_fast_cluster_kernel(CbParams P) {
+  cg::grid_group grid = cg::this_grid();
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ CbShared sh;
+  __shared__ CbFastCand s_fc[kCbThreads / 32];
+  __shared__ CbFastCand s_ccand;
+  __shared__ double s_cthr[2];
+  __shared__ int s_stop, s_feat;
+  __shared__ double s_alpha, s_thr, s_pol, s_err;
+
+  const int n = P.n, F = P.F, cl = P.cl;
+  const int r = (int)cluster.block_rank();
+  const int f = blockIdx.x / cl;
+  const int n_pos_all = *P.n_pos;
+  if (one_class_exit(P.raw, n, n_pos_all, P.out_count, P.out_intercept)) return;
+  const int L = P.n_leaves;
+  const int qt = P.qt;
+  const int cblock = qt * kCbThreads;
+  const int ctile = cl * cblock;
+  const int n_tiles = (n + ctile - 1) / ctile;
+  double *s_node = reinterpret_cast<double *>(smem_raw);
+  double *s_leaf = s_node + 2 * L;
+  double *s_leaf_b = s_leaf + L;
+  double *wsl = s_leaf + 2 * L;
+  unsigned *s_code = reinterpret_cast<unsigned *>(wsl + P.slice_cap);
+  signed char *s_y = reinterpret_cast<signed char *>(s_code + P.pos_cap);
+  int2 *s_leaves = reinterpret_cast<int2 *>(smem_raw + ((sizeof(double) * (4 * (size_t)L + P.slice_cap) +
+                                                         sizeof(unsigned) * P.pos_cap + P.slice_cap + 15) &
+                                                        ~(size_t)15));
+  int2 *s_children = s_leaves + L;
+  int *s_level = reinterpret_cast<int *>(s_children + max(L - 1, 0));
+  for (int i = threadIdx.x; i < L; i += blockDim.x) s_leaves[i] = P.leaves[i];
+  for (int i = threadIdx.x; i < L - 1; i += blockDim.x) s_children[i] = P.children[i];
+  for (int i = threadIdx.x; i < P.n_levels; i += blockDim.x) s_level[i] = P.level_end[i];
+  const PwView T{s_leaves, s_children, s_level, L, P.n_levels, P.root};
+  int l_lo, l_hi;
+  cb_leaf_run(L, cl, r, l_lo, l_hi);
+  const int e_lo = l_lo < L ? P.leaves[l_lo].x : n;
+  const int e_hi = l_hi > l_lo ? P.leaves[l_hi - 1].x + P.leaves[l_hi - 1].y : e_lo;
+  double *wloc = wsl - e_lo;
+  const unsigned *code = P.code + (size_t)f * n;
+  for (int t = 0; t < n_tiles; ++t)
+    for (int j = threadIdx.x; j < cblock; j += blockDim.x) {
+      const int i = t * ctile + r * cblock + j;
+      if (i < n) s_code[t * cblock + j] = __ldg(code + i);
+    }
+  for (int i = e_lo + (int)threadIdx.x; i < e_hi; i += blockDim.x) s_y[i - e_lo] = P.y[i] > 0.0 ? 1 : -1;
+  if (threadIdx.x <= kCbMaxCluster) {
+    const int o = threadIdx.x;
+    int lo = 0, hi = 0;
+    cb_leaf_run(L, cl, min(o, cl - 1), lo, hi);
+    sh.elo[o] = o >= cl ? n : (lo < L ? P.leaves[lo].x : n);
+    if (o < cl) sh.rw[o] = cluster.map_shared_rank(wsl, o) - sh.elo[o];
+  }
+  int count = 0;
+  __syncthreads();
+  pw_leaf_sums(T, P.w0, l_lo, l_hi, s_leaf, PwIdentity{}, [&](int i, double v) { wloc[i] = v; });
+  double ssum = cb_tree(cluster, T, s_leaf, s_node, cl);
+
+  for (int round = 0; round < P.rounds; ++round) {
+    const double inv_s = 1.0 / ssum;
+    // ---- integer split scan of feature f over the cluster -----------------
+    long long dmin = LLONG_MAX, dmax = LLONG_MIN;
+    int kmin = INT_MAX, kmax = INT_MAX;
+    long long carry_p = 0, carry_n = 0;
+    for (int t0 = 0, tile = 0; t0 < n; t0 += ctile, ++tile) {
+      const int i0 = t0 + r * cblock + threadIdx.x * qt;
+      const int q = max(0, min(qt, n - i0));
+      const unsigned *tc = s_code + tile * cblock + threadIdx.x * qt;
+      long long W[kCbQ];
+      unsigned neg_mask = 0, brk_mask = 0;
+      CbScanL mine{0, 0, 0, 0};
+#pragma unroll
+      for (int k = 0; k < kCbQ; ++k) {
+        W[k] = 0;
+        if (k < q) {
+          const unsigned c = tc[k];
+          W[k] = __double2ll_rn(cb_weight(sh, cl, (int)(c & kCodeId)) * inv_s * kFixC);
+          if (c & kCodeNeg) {
+            neg_mask |= 1u << k;
+            mine.p1 += W[k];
+          } else {
+            mine.p0 += W[k];
+          }
+          if (c & kCodeBrk) brk_mask |= 1u << k;
+        }
+      }
+      CbScanL tl;
+      const CbScanL ex = cb_scan_l(mine, sh.s_l, tl);
+      if (threadIdx.x == 0) sh.tot_l = tl;
+      cluster.sync();
+      long long bp = carry_p, bn = carry_n, ap = 0, an = 0;
+      for (int o = 0; o < cl; ++o) {
+        const CbScanL to = cluster.map_shared_rank(&sh, o)->tot_l;
+        if (o < r) {
+          bp += to.p0;
+          bn += to.p1;
+        }
+        ap += to.p0;
+        an += to.p1;
+      }
+      long long cp = bp + ex.p0, cn = bn + ex.p1;
+#pragma unroll
+      for (int k = 0; k < kCbQ; ++k) {
+        if (k < q) {
+          if ((neg_mask >> k) & 1u) cn += W[k];
+          else cp += W[k];
+          const int i = i0 + k;
+          if (((brk_mask >> k) & 1u) && i < n - 1) {
+            const long long dd = cp - cn;
+            if (dd < dmin) dmin = dd, kmin = 2 * i;  // positions ascend: first hit keeps the lowest key
+            if (dd > dmax) dmax = dd, kmax = 2 * i + 1;
+          }
+        }
+      }
+      carry_p += ap;
+      carry_n += an;
+      cluster.sync();  // tot_l is reused by the next tile
+    }
+    const long long tot_pos = carry_p, tot_neg = carry_n, total = tot_pos + tot_neg;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const long long o1 = __shfl_down_sync(0xffffffffu, dmin, off), o2 = __shfl_down_sync(0xffffffffu, dmax, off);
+      const int k1 = __shfl_down_sync(0xffffffffu, kmin, off), k2 = __shfl_down_sync(0xffffffffu, kmax, off);
+      if (o1 < dmin || (o1 == dmin && k1 < kmin)) dmin = o1, kmin = k1;
+      if (o2 > dmax || (o2 == dmax && k2 < kmax)) dmax = o2, kmax = k2;
+    }
+    if ((threadIdx.x & 31) == 0) s_fc[threadIdx.x >> 5] = CbFastCand{dmin, dmax, kmin, kmax};
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      CbFastCand c = s_fc[0];
+      for (int w = 1; w < (int)blockDim.x / 32; ++w) {
+        const CbFastCand o = s_fc[w];
+        if (o.dmin < c.dmin || (o.dmin == c.dmin && o.kmin < c.kmin)) c.dmin = o.dmin, c.kmin = o.kmin;
+        if (o.dmax > c.dmax || (o.dmax == c.dmax && o.kmax < c.kmax)) c.dmax = o.dmax, c.kmax = o.kmax;
+      }
+      s_ccand = c;
+    }
+    cluster.sync();
+    if (r == 0 && threadIdx.x == 0) {
+      CbFastCand c = s_ccand;
+      for (int o = 1; o < cl; ++o) {
+        const CbFastCand oc = *cluster.map_shared_rank(&s_ccand, o);
+        if (oc.dmin < c.dmin || (oc.dmin == c.dmin && oc.kmin < c.kmin)) c.dmin = oc.dmin, c.kmin = oc.kmin;
+        if (oc.dmax > c.dmax || (oc.dmax == c.dmax && oc.kmax < c.kmax)) c.dmax = oc.dmax, c.kmax = oc.kmax;
+      }
+      // err+ = d + tot_neg, err- = tot_pos - d; lowest key at equal error
+      long long best_err = LLONG_MAX;
+      int best_key = INT_MAX;
+      if (c.kmin != INT_MAX) best_err = c.dmin + tot_neg, best_key = c.kmin;
+      if (c.kmax != INT_MAX) {
+        const long long em = tot_pos - c.dmax;
+        if (em < best_err || (em == best_err && c.kmax < best_key)) best_err = em, best_key = c.kmax;
+      }
+      double thr = 0.0;
+      if (best_key != INT_MAX) {
+        const double *xf = P.xsorted + (size_t)f * n;
+        const int i = best_key >> 1;
+        thr = 0.5 * (xf[i] + xf[i + 1]);
+      }
+      P.feat_ierr[(round & 1) * F + f] = best_err;
+      P.feat_pos[(round & 1) * F + f] = best_key;
+      P.feat_thr[(round & 1) * F + f] = thr;
+    }
+    grid.sync();
+    // ---- the winner (every CTA, same answer) -----------------------------
+    if (threadIdx.x == 0) {
+      const long long *ferr = P.feat_ierr + (round & 1) * F;
+      long long be = LLONG_MAX;
+      int bf = -1, bk = 0;
+      double bt = 0.0;
+      for (int g = 0; g < F; ++g) {
+        const int pos = __ldcg(P.feat_pos + (round & 1) * F + g);
+        const long long e = __ldcg(ferr + g);
+        if (pos != INT_MAX && e < be) be = e, bf = g, bk = pos, bt = __ldcg(P.feat_thr + (round & 1) * F + g);
+      }
+      if (bf < 0) {  // every feature constant: majority constant stump
+        const double pol = 2 * tot_neg <= total ? 1.0 : -1.0;  // +1 iff sum(w y) >= 0
+        s_feat = 0;
+        s_thr = __longlong_as_double(0xfff0000000000000LL);
+        s_pol = pol;
+        s_err = (double)(pol > 0 ? tot_neg : total - tot_neg) / (double)total;
+      } else {
+        s_feat = bf;
+        s_thr = bt;
+        s_pol = (bk & 1) ? -1.0 : 1.0;
+        s_err = (double)be / (double)total;
+      }
+      const double err = s_err;
+      if (P.raw) {
+        if (blockIdx.x == 0) {
+          P.out_feat[0] = s_feat, P.out_thr[0] = s_thr, P.out_pol[0] = s_pol, P.out_alpha[0] = 1.0;
+          P.out_err[0] = err;
+        }
+        s_stop = 3;
+      } else if (err >= 0.5) {
+        s_stop = 1;
+      } else {
+        const double a = 0.5 * log((1.0 - err) / (err > 1e-10 ? err : 1e-10));
+        s_alpha = a;
+        if (blockIdx.x == 0) {
+          P.out_feat[count] = s_feat, P.out_thr[count] = s_thr, P.out_pol[count] = s_pol;
+          P.out_alpha[count] = a, P.out_err[count] = err;
+        }
+        s_stop = err <= 0.0 ? 3 : 0;
+      }
+    }
+    __syncthreads();
+    if (s_stop == 1) break;
+    ++count;
+    if (s_stop == 3 || round + 1 == P.rounds) break;
+    // ---- reweight this CTA's leaf run; new pairwise sum ---------------------
+    {
+      const double a = s_alpha, thr = s_thr, pol = s_pol;
+      const double *xcol = P.xt + (size_t)s_feat * n;
+      const double e_agree = exp(-a), e_miss = exp(a);
+      double *buf = (round & 1) ? s_leaf : s_leaf_b;  // alternate the leaf-sum buffers (see cb_tree)
+      pw_leaf_sums(
+          T, wloc, l_lo, l_hi, buf,
+          [&](int i, double x) {
+            const double pred = __ldg(xcol + i) > thr ? pol : -pol;
+            return x * inv_s * (((double)s_y[i - e_lo] * pred > 0.0) ? e_agree : e_miss);
+          },
+          [&](int i, double v) { wloc[i] = v; });
+      ssum = cb_tree(cluster, T, buf, s_node, cl);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) write_result(count, n, n_pos_all, P.out_count, P.out_intercept);
+  cluster.sync();
 }
 
 }  // namespace brm
