@@ -749,12 +749,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
           lc.numAttrs = 1;
           break;
         }
-        int max_clusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&max_clusters, kfn, &lc) != cudaSuccess) {
-          cudaGetLastError();
-          max_clusters = 0;
-        }
-        if (max_clusters >= F || cl == 1) break;
+        if (max_active_clusters(kfn, lc, device) >= F || cl == 1) break;
       }
       P.cl = cl;
       P.qt = (int)std::min<int64_t>(kCbQ, ((int64_t)n + (int64_t)cl * kCbThreads - 1) / ((int64_t)cl * kCbThreads));

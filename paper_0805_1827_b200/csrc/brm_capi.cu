@@ -185,10 +185,12 @@ int fetch(const T *src, size_t count, std::vector<T> &dst, const char *name) {
 
 int quad_basis_size(int k) { return 1 + k + k * (k + 1) / 2; }
 
+}  // namespace
+
 // cudaOccupancyMaxActiveClusters, cached per (kernel, cluster size, block,
 // dynamic shared memory, device): the query costs tens of microseconds and
-// the per-date probe launches would repeat it.
-int max_active_clusters(const void *kernel, const cudaLaunchConfig_t &cfg, int device) {
+// the per-date probe / AdaBoost launches would repeat it.
+int brm::max_active_clusters(const void *kernel, const cudaLaunchConfig_t &cfg, int device) {
   static std::mutex mu;
   static std::map<std::tuple<const void *, int, int, size_t, int>, int> cache;
   int csize = 1;
@@ -209,6 +211,8 @@ int max_active_clusters(const void *kernel, const cudaLaunchConfig_t &cfg, int d
   cache[key] = v;
   return v;
 }
+
+namespace {
 
 }  // namespace
 

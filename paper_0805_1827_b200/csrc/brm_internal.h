@@ -154,6 +154,9 @@ int launch_ls_fit(const LsParams &P, int n_fits, cudaStream_t s);
 size_t ls_fit_smem(int J, int nb);
 size_t set_ensemble_smem(int capacity);
 
+// Cached cudaOccupancyMaxActiveClusters for a launch configuration (brm_capi.cu).
+int max_active_clusters(const void *kernel, const cudaLaunchConfig_t &cfg, int device);
+
 // Keep freed stream-ordered allocations in the device's default pool across
 // synchronisations (the pool's default release threshold of 0 hands them back
 // to the driver at every sync, and the next call re-maps them).
