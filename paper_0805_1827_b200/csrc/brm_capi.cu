@@ -277,8 +277,13 @@ int smem_model(const brm_ctx *c) {
   return c->fast() ? model_smem_bytes<float>(c->hdr) : model_smem_bytes<double>(c->hdr);
 }
 
+// Opt in to `bytes` of dynamic shared memory and ask for the largest shared
+// carve-out: the walkers' residency is a register / shared-memory trade, and
+// the driver's default carve-out only fits the CTAs it predicts, which caps
+// a 3-CTA-per-SM instance at 2.
 int allow_smem(const void *kernel, int bytes) {
   BRM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  BRM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   return BRM_OK;
 }
 
@@ -334,19 +339,29 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   P.nrm_count = c->nrm_count;
   P.path_out = j.path_out;
   P.stop_out = j.stop_out;
-  P.vals_offset = smem_model(c);
   P.steps = step_counter(PK_WALK);
-  const int smem = P.vals_offset + 8 * P.chunk;
-  if (smem > c->info.max_smem) return fail(BRM_EINVAL, "model image too large for shared memory (%d B)", smem);
-  BRM_TRY(call.scratch<double>(2 * (size_t)P.n_items, &P.partials));
   // the CMC instance assumes even draw indices at every step for even d (parity mode)
   const bool even_ok = c->fast() || c->hdr.d % 2 == 1 || (P.draw_base % 2 == 0);
   void *kwalk = c->kern.walk;
+  P.vals_offset = smem_model(c);
   if (c->hdr.rule == BRM_RULE_CMC && !P.normals && even_ok) {
-    if (c->hdr.unit_diag && c->hdr.payoff == BRM_PAY_MAXCALL && c->kern.walk_cmc_unit) kwalk = c->kern.walk_cmc_unit;
-    else if (c->fast() && c->hdr.chol_lower == 1 && c->kern.walk_cmc_lower) kwalk = c->kern.walk_cmc_lower;
-    else if (c->kern.walk_cmc) kwalk = c->kern.walk_cmc;
+    // parity mode walks log-prices (brm_walk_log.cuh); BRM_WALK_LOG=0 keeps the price stepper (A/B runs)
+    static const bool log_walk = !(std::getenv("BRM_WALK_LOG") && std::getenv("BRM_WALK_LOG")[0] == '0');
+    const bool maxcall_unit = c->hdr.unit_diag && c->hdr.payoff == BRM_PAY_MAXCALL;
+    if (maxcall_unit && !c->fast() && log_walk && c->kern.walk_cmc_log && c->hdr.n_dates <= 255) {
+      kwalk = c->kern.walk_cmc_log;
+      P.vals_offset = log_model_smem_bytes(c->hdr);  // search trees instead of the bucket tables
+    } else if (maxcall_unit && c->kern.walk_cmc_unit) {
+      kwalk = c->kern.walk_cmc_unit;
+    } else if (c->fast() && c->hdr.chol_lower == 1 && c->kern.walk_cmc_lower) {
+      kwalk = c->kern.walk_cmc_lower;
+    } else if (c->kern.walk_cmc) {
+      kwalk = c->kern.walk_cmc;
+    }
   }
+  const int smem = P.vals_offset + 8 * P.chunk;
+  if (smem > c->info.max_smem) return fail(BRM_EINVAL, "model image too large for shared memory (%d B)", smem);
+  BRM_TRY(call.scratch<double>(2 * (size_t)P.n_items, &P.partials));
   BRM_TRY(allow_smem(kwalk, smem));
   int per_sm = 0;
   BRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kwalk, kWalkThreads, smem));

@@ -106,6 +106,7 @@ struct KernelTriple {
   void *walk_cmc = nullptr;       // walker specialised for CMC rules (d > 1)
   void *walk_cmc_unit = nullptr;  // ... max-call payoff, independent assets (unit diagonal factor)
   void *walk_cmc_lower = nullptr; // ... fast mode, lower-triangular factor
+  void *walk_cmc_log = nullptr;   // ... walk_cmc_unit's case in parity mode on log-prices (brm_walk_log.cuh)
 };
 
 // Kernel families for launch accounting (brm_prof.cu, BRM_PROF_* in the C ABI).

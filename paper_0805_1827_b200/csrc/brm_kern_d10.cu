@@ -9,6 +9,7 @@ KernelTriple kernels_d10(bool fast) {
                         (void *)&walk_units<10, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<10, false>, (void *)&iz_probes<10, false>, (void *)&decisions<10, false>,
                       (void *)&iz_probes<10, false, true>, (void *)&walk_units<10, false, WALK_CMC>,
-                      (void *)&walk_units<10, false, WALK_CMC_UNIT>};
+                      (void *)&walk_units<10, false, WALK_CMC_UNIT>, nullptr,
+                      (void *)&walk_units<10, false, WALK_CMC_LOG>};
 }
 }  // namespace brm

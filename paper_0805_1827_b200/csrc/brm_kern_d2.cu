@@ -9,6 +9,7 @@ KernelTriple kernels_d2(bool fast) {
                         (void *)&walk_units<2, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<2, false>, (void *)&iz_probes<2, false>, (void *)&decisions<2, false>,
                       (void *)&iz_probes<2, false, true>, (void *)&walk_units<2, false, WALK_CMC>,
-                      (void *)&walk_units<2, false, WALK_CMC_UNIT>};
+                      (void *)&walk_units<2, false, WALK_CMC_UNIT>, nullptr,
+                      (void *)&walk_units<2, false, WALK_CMC_LOG>};
 }
 }  // namespace brm

@@ -9,6 +9,7 @@ KernelTriple kernels_d3(bool fast) {
                         (void *)&walk_units<3, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<3, false>, (void *)&iz_probes<3, false>, (void *)&decisions<3, false>,
                       (void *)&iz_probes<3, false, true>, (void *)&walk_units<3, false, WALK_CMC>,
-                      (void *)&walk_units<3, false, WALK_CMC_UNIT>};
+                      (void *)&walk_units<3, false, WALK_CMC_UNIT>, nullptr,
+                      (void *)&walk_units<3, false, WALK_CMC_LOG>};
 }
 }  // namespace brm

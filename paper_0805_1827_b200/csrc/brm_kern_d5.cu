@@ -9,6 +9,7 @@ KernelTriple kernels_d5(bool fast) {
                         (void *)&walk_units<5, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<5, false>, (void *)&iz_probes<5, false>, (void *)&decisions<5, false>,
                       (void *)&iz_probes<5, false, true>, (void *)&walk_units<5, false, WALK_CMC>,
-                      (void *)&walk_units<5, false, WALK_CMC_UNIT>};
+                      (void *)&walk_units<5, false, WALK_CMC_UNIT>, nullptr,
+                      (void *)&walk_units<5, false, WALK_CMC_LOG>};
 }
 }  // namespace brm

@@ -16,14 +16,21 @@
 
 #include "brm_internal.h"
 #include "brm_walk.cuh"
+#include "brm_walk_log.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace brm {
 
 // ---------------------------------------------------------------- walk ----
+#ifndef BRM_LOG_MINB
+#define BRM_LOG_MINB 2
+#endif
 template <int D, bool FAST, int SPEC = WALK_GENERIC>
-__global__ void __launch_bounds__(kWalkThreads, (FAST && D < 20) ? 3 : 2) walk_units(WalkParams P) {
+__global__ void __launch_bounds__(kWalkThreads, SPEC == WALK_CMC_LOG ? BRM_LOG_MINB : ((FAST && D < 20) ? 3 : 2))
+    walk_units(WalkParams P) {
+  constexpr bool kLog = SPEC == WALK_CMC_LOG;  // log-price state and log-threshold tables (brm_walk_log.cuh)
+  static_assert(!kLog || (!FAST && D > 1), "the log-price walker is a parity instance for d > 1");
   constexpr int TG = FAST ? 1 : TailGroup<D>::G;
   __shared__ double s_tq_buf[(kWalkThreads / 32) * 32 * TG];
   __shared__ unsigned short s_tq_idx[(kWalkThreads / 32) * 32 * TG];
@@ -33,9 +40,11 @@ __global__ void __launch_bounds__(kWalkThreads, (FAST && D < 20) ? 3 : 2) walk_u
   __shared__ double s_red[2 * (kWalkThreads / 32)];
   __shared__ int s_next;
   __shared__ R s_start[kMaxD];
-  const Model<R> M = load_model<R>(P.hdr, P.blob, smem);
+  __shared__ unsigned char s_stopm[kLog ? kMaxChunk : 1];  // log-price walker: stop date per path slot
+  const Model<R> M = load_model<R, kLog>(P.hdr, P.blob, smem);
   double *vals = reinterpret_cast<double *>(smem + P.vals_offset);
   const int d = M.d;
+  [[maybe_unused]] const double log_strike = kLog ? log(P.hdr.strike) : 0.0;
   // the specialised instances never run on supplied normals (host check)
   const NormalSrc ns = SPEC == WALK_GENERIC ? NormalSrc{P.normals, P.nrm_base, P.nrm_count} : NormalSrc{nullptr, 0, 0};
 
@@ -54,16 +63,25 @@ __global__ void __launch_bounds__(kWalkThreads, (FAST && D < 20) ? 3 : 2) walk_u
       derive_words(P.seed, (uint64_t)P.phase, (uint64_t)(P.item_base + u), (uint64_t)P.key_date, key, stream);
     }
     __syncthreads();  // previous item finished with s_start / vals / s_next
-    if (threadIdx.x < d) s_start[threadIdx.x] = P.starts ? (R)P.starts[(size_t)u * P.start_stride + threadIdx.x]
-                                                         : M.s0[threadIdx.x];
+    if (threadIdx.x < d) {
+      const R s = P.starts ? (R)P.starts[(size_t)u * P.start_stride + threadIdx.x] : M.s0[threadIdx.x];
+      if constexpr (kLog) s_start[threadIdx.x] = log(s);
+      else s_start[threadIdx.x] = s;
+    }
     if (threadIdx.x == 0) s_next = p0 + blockDim.x;
     __syncthreads();
     if (p0 < p1) {
       const uint64_t base0 = unit_base<FAST>(P.draw_base, P.normals != nullptr);
       double *pout = P.path_out ? P.path_out + (size_t)u * P.per_unit : nullptr;
       int32_t *sout = P.stop_out ? P.stop_out + (size_t)u * P.per_unit : nullptr;
-      walk_paths<D, FAST, SPEC>(M, s_start, P.m_start, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, pout,
-                          sout, P.steps, tq);
+      if constexpr (kLog) {
+        walk_paths_log<(D > 1 ? D : 2)>(M, s_start, log_strike, P.m_start, P.n_steps, key, stream, base0, p0, p1, vals,
+                                        s_stopm, &s_next, P.steps, tq);
+        __syncthreads();
+        finish_log_values(M, P.m_start, p0, p1 - p0, vals, s_stopm, pout, sout);
+      } else
+        walk_paths<D, FAST, SPEC>(M, s_start, P.m_start, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, pout,
+                                  sout, P.steps, tq);
     }
     __syncthreads();
     double s = 0.0, q = 0.0;

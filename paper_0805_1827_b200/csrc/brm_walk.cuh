@@ -96,8 +96,10 @@ __device__ __forceinline__ double geo_payoff(const Model<double> &M, const doubl
 // WALK_GEO: the geometric put (geo_payoff); WALK_CMC: a CMC rule (the
 // labels and pricing of C3-C5); WALK_CMC_UNIT: the max-call payoff under a
 // CMC rule with independent assets (unit diagonal factor: C3, C5);
-// WALK_CMC_LOWER: fast mode, CMC rule, lower-triangular factor (C4).
-enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_CMC = 2, WALK_CMC_UNIT = 3, WALK_CMC_LOWER = 4 };
+// WALK_CMC_LOWER: fast mode, CMC rule, lower-triangular factor (C4);
+// WALK_CMC_LOG: WALK_CMC_UNIT's case in parity mode with the state kept as
+// log-prices (brm_walk_log.cuh).
+enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_CMC = 2, WALK_CMC_UNIT = 3, WALK_CMC_LOWER = 4, WALK_CMC_LOG = 5 };
 
 template <int D, bool FAST, int SPEC = WALK_GENERIC>
 __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_start, int m_start, int n_steps,

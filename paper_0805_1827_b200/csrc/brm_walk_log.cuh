@@ -1,0 +1,269 @@
+// brm_walk_log.cuh -- the log-price walker instance (WALK_CMC_LOG): max-call
+// payoff, CMC rule, independent assets, parity draws (C3 / C5 in fp64).
+//
+// The reference's _path_value (_core.pyx:290-323) steps prices,
+// v_i <- v_i * exp(mu_i + vol_i z_i), and needs d exponentials per step.  For
+// this payoff and rule nothing on the path needs the prices themselves:
+//   * the max-call payoff is max_i v_i - K, and max_i v_i = exp(max_i x_i)
+//     for x_i = log v_i, so "payoff > 0" is x_max > log K and the payoff value
+//     is needed once per path, at the stop date;
+//   * a stump asks v_f > t, which is x_f > log t (the derived feature
+//     max_i v_i likewise), so the rule's step functions are searched over
+//     log-thresholds (build_log_tables, brm_model.cuh).
+// The state therefore is the log-price, x_i <- x_i + (mu_i + vol_i z_i): two
+// fp64 operations per asset-step where the price step costs ~20, and one
+// exponential per path.  Draws are the reference's (Philox + AS241, the same
+// draw indices), so the log-prices differ from the logs of the reference's
+// prices only by rounding (a few 1e-16 relative in the price; the K-scaled
+// 1e-12 parity tolerance of DESIGN.md section 4 holds with three orders of
+// margin), and a decision can differ only for a state within that rounding of
+// a threshold -- the same caveat the price stepper already carries, because
+// CUDA's exp and glibc's differ in the last bit.
+//
+// Exactness guards: "in the money" within 1e-13 of log K and stump scores
+// inside the rounding bound bound[m] are decided in price space from
+// exp(x) (rare branches), so the decision is the price-space decision of the
+// state exp(x) whenever the cheap test cannot be trusted.
+//
+// A stopped path leaves (x_max, stop date) in its shared-memory slot; the
+// payoff (exp(x_max) - K) disc is formed afterwards by all lanes of the CTA
+// (finish_log_values) instead of by the two or three lanes of a warp that
+// stop in a given step.
+#pragma once
+#include "brm_walk.cuh"
+
+namespace brm {
+
+// Stump score of the state exp(x) in stump order (the reference's sequential
+// sum, _core.pyx:271-287); reached only when the table sum is inside bound[m]
+// or the search trees did not fit in shared memory.
+template <int D>
+__device__ __forceinline__ bool cmc_stop_exact_log(const Model<double> &M, int m, const double *x, double xmax) {
+  double v_of[D + 1];
+#pragma unroll
+  for (int i = 0; i < D; ++i) v_of[i] = exp_nb(x[i]);
+  v_of[D] = exp_nb(xmax);
+  double s = M.icept[m];
+  const int t0 = M.starts[m], t1 = t0 + M.counts[m];
+  for (int t = t0; t < t1; ++t) {
+    const double v = v_of[M.feat[t]];
+    s = v > M.thr[t] ? r_add(s, M.ap[t]) : r_sub(s, M.ap[t]);
+  }
+  return s > 0.0;
+}
+
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+// Stump score through the per-feature search trees (build_log_tables): D + 1
+// branch-free searches in lock-step, then a pairwise sum.  The sum is in a
+// different order than the reference's, so it decides only outside the
+// rounding bound bound[m] (see cmc_stop, brm_model.cuh).
+template <int D>
+__device__ __forceinline__ bool cmc_stop_log(const Model<double> &M, int m, const double *x, double xmax) {
+  if (M.lt_base == 0) return cmc_stop_exact_log<D>(M, m, x, xmax);  // uniform
+  constexpr int FN = D + 1;
+  // a[f]: byte address of the current node; a <- 2a + (8 - base) + 8 [node < x]
+  unsigned a[FN], kf[FN];
+  const unsigned date = M.lt_base + (unsigned)(m - 1) * (unsigned)M.lt_date;
+#pragma unroll
+  for (int f = 0; f < FN; ++f) {
+    a[f] = date + (unsigned)f * (unsigned)M.lt_s1;
+    kf[f] = 8u - a[f];
+  }
+  const int dmin = min(M.lt_d1, M.lt_d2);
+#pragma unroll 1
+  for (int l = 0; l < dmin; ++l) {
+    double t[FN];
+#pragma unroll
+    for (int f = 0; f < FN; ++f) t[f] = lds_f64(a[f]);
+#pragma unroll
+    for (int f = 0; f < FN; ++f) a[f] = 2u * a[f] + kf[f] + (t[f] < (f < D ? x[f < D ? f : 0] : xmax) ? 8u : 0u);
+  }
+#pragma unroll 1
+  for (int l = dmin; l < M.lt_d1; ++l) {  // deeper asset trees
+    double t[D];
+#pragma unroll
+    for (int f = 0; f < D; ++f) t[f] = lds_f64(a[f]);
+#pragma unroll
+    for (int f = 0; f < D; ++f) a[f] = 2u * a[f] + kf[f] + (t[f] < x[f] ? 8u : 0u);
+  }
+#pragma unroll 1
+  for (int l = dmin; l < M.lt_d2; ++l)  // deeper derived-feature tree
+    a[D] = 2u * a[D] + kf[D] + (lds_f64(a[D]) < xmax ? 8u : 0u);
+  double val[FN];
+#pragma unroll
+  for (int f = 0; f < FN; ++f) val[f] = lds_f64(a[f]);
+#pragma unroll
+  for (int w = 1; w < FN; w <<= 1)
+#pragma unroll
+    for (int f = 0; f + w < FN; f += 2 * w) val[f] = r_add(val[f], val[f + w]);
+  const double s = r_add(M.icept[m], val[0]);
+  const double B = M.bound[m];
+  if (s > B) return true;
+  if (s < -B) return false;
+  return cmc_stop_exact_log<D>(M, m, x, xmax);
+}
+
+// Parity draws of one step, consumed group by group: after a group's normals
+// are final (central branch per lane, tail draws through the warp queue, as
+// step_draws_compact) the log-prices of the group's assets step at once, so
+// only one group of normals is live.  Queue slots come from one ballot per
+// draw (the rank of the lane among the lanes whose draw is a tail draw).
+template <int D, bool EVEN>
+__device__ __forceinline__ void step_log_prices(const Model<double> &M, const PhiloxKey &K, uint64_t idx0, double *x,
+                                                bool active, double *wbuf, unsigned short *widx, unsigned lt_mask) {
+  constexpr int NC = EVEN ? D / 2 : D / 2 + 1;
+  constexpr int G = TailGroup<D>::G;
+  static_assert(D % G == 0, "the log-price walker steps whole draw groups");
+  const uint64_t c0 = idx0 >> 1;
+  const bool odd = EVEN ? false : (idx0 & 1);
+  const int ncalls = EVEN ? NC : (int)(((idx0 + D - 1) >> 1) - c0) + 1;
+  double z[D];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    if (j < ncalls) {
+      const Philox4 p = philox(K, c0 + j);
+      const double u0 = uniform_x2(philox_word(p, 0)), u1 = uniform_x2(philox_word(p, 1));
+      if (2 * j < D) z[2 * j] = odd ? u1 : u0;
+      if (2 * j + 1 < D && !odd) z[2 * j + 1] = u1;
+      if (j > 0 && 2 * j - 1 < D && odd) z[2 * j - 1] = u0;
+    }
+  }
+  const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int g0 = 0; g0 < D; g0 += G) {
+    bool tail[G];
+    int total = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const double q = fma(z[g0 + g], 0x1p-54, -0.5);
+      const bool central = fabs(q) <= 0.425;
+      tail[g] = !central && active;
+      const double c = as241_central(q);
+      if (central) z[g0 + g] = c;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const unsigned mask = __ballot_sync(0xffffffffu, tail[g]);
+      if (tail[g]) {
+        const int slot = lane * G + g;
+        wbuf[slot] = z[g0 + g];
+        widx[total + __popc(mask & lt_mask)] = (unsigned short)slot;
+      }
+      total += __popc(mask);
+    }
+    if (total != 0) {
+      __syncwarp();
+      for (int j = lane; j < total; j += 32) {
+        const int slot = widx[j];
+        const double u = __dmul_rn(wbuf[slot], 0x1p-54);  // exact
+        wbuf[slot] = as241_tail(u, __dsub_rn(u, 0.5));
+      }
+      __syncwarp();
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (tail[g]) z[g0 + g] = wbuf[lane * G + g];
+      __syncwarp();
+    }
+#pragma unroll
+    for (int a = g0; a < g0 + G; ++a) x[a] = r_add(x[a], fma(M.vol[a], z[a], M.mu[a]));
+  }
+}
+
+// Walk paths [p0, p1) of one unit from the shared start log-prices x_start
+// (lane refill as walk_paths, brm_walk.cuh).  Slot p - p0 of vals receives the
+// stopped path's x_max and stopm its stop date (0: expired worthless);
+// finish_log_values turns them into discounted payoffs.
+template <int D>
+__device__ void walk_paths_log(const Model<double> &M, const double *x_start, double log_strike, int m_start,
+                               int n_steps, uint64_t key, uint64_t stream, uint64_t base0, int p0, int p1,
+                               double *vals, unsigned char *stopm, int *s_next, unsigned long long *step_count,
+                               const TailQueue &tq) {
+  static_assert(D > 1, "the log-price walker is the d > 1 max-call instance");
+  const uint64_t stride = (uint64_t)n_steps * (uint64_t)D;
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const PhiloxKey K = philox_key(key, stream);
+  double x[D];
+
+  unsigned nsteps = 0;
+  int p = p0 + threadIdx.x;
+  bool have = p < p1;
+  int k = 0;
+  uint64_t base = base0 + (uint64_t)(have ? p : 0) * stride;
+#pragma unroll
+  for (int i = 0; i < D; ++i) x[i] = x_start[i];
+
+  while (__any_sync(0xffffffffu, have)) {
+    bool done = false;
+    double xstop = 0.0;
+    int stop_m = 0;
+    // the whole warp draws (the tail pass is warp-cooperative); lanes without
+    // a path step a dummy state at a valid index and discard it
+    step_log_prices<D, D % 2 == 0>(M, K, base + (uint64_t)k * (uint64_t)D, x, have, tq.buf, tq.idx, lt_mask);
+    if (have) {
+      ++nsteps;
+      const int m = m_start + k + 1;
+      double xmax = x[0];
+#pragma unroll
+      for (int i = 1; i < D; ++i)
+        if (x[i] > xmax) xmax = x[i];
+      const double dk = r_sub(xmax, log_strike);
+      bool itm = dk > 0.0;
+      if (fabs(dk) <= 1e-13) itm = r_sub(exp_nb(xmax), M.strike) > 0.0;  // decide at the money in price space
+      if (itm && (m == M.n_dates || cmc_stop_log<D>(M, m, x, xmax))) {
+        xstop = xmax;
+        stop_m = m;
+        done = true;
+      } else if (k + 1 == n_steps) {
+        done = true;
+      } else {
+        ++k;
+      }
+    }
+    if (done) {
+      vals[p - p0] = xstop;
+      stopm[p - p0] = (unsigned char)stop_m;
+    }
+    const unsigned need = __ballot_sync(0xffffffffu, done);
+    if (need) {
+      const int leader = __ffs(need) - 1;
+      int got = 0;
+      if ((int)lane == leader) got = atomicAdd(s_next, __popc(need));
+      got = __shfl_sync(0xffffffffu, got, leader);
+      if (done) {
+        p = got + __popc(need & lt_mask);
+        have = p < p1;
+        k = 0;
+        base = base0 + (uint64_t)(have ? p : 0) * stride;
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = x_start[i];
+      }
+    }
+  }
+  if (step_count) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) nsteps += __shfl_down_sync(0xffffffffu, nsteps, off);
+    if (lane == 0 && nsteps) atomicAdd(step_count, (unsigned long long)nsteps);
+  }
+}
+
+// (x_max, stop date) of every path of the chunk -> discounted payoff
+// (exp(x_max) - K) disc[m - m_start] in place, and the optional per-path
+// outputs.  All threads; the caller synchronises before and after.
+__device__ __forceinline__ void finish_log_values(const Model<double> &M, int m_start, int p0, int n, double *vals,
+                                                  const unsigned char *stopm, double *path_out, int32_t *stop_out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int m = stopm[i];
+    const double v = m ? r_mul(r_sub(exp_nb(vals[i]), M.strike), M.disc[m - m_start]) : 0.0;
+    vals[i] = v;
+    if (path_out) path_out[p0 + i] = v;
+    if (stop_out) stop_out[p0 + i] = m;
+  }
+}
+
+}  // namespace brm
