@@ -57,12 +57,15 @@ CONFIGS = {
 # This is the work the roofline counts, independent of this build's SASS.
 DP_OPS_PER_ASSET_STEP = 70.0
 # What the walker actually executes on the fp64 pipe (ncu: DADD+DMUL+DFMA+DSETP
-# thread instructions / executed asset-steps on the C5 label launch,
-# profiles/r01d_walk_c5_sass_mix.txt): reported beside it as overhead.
-DP_OPS_EXECUTED_NCU = 80.7
+# thread instructions / executed asset-steps on the C5 label launch of the
+# log-price walker, profiles/r02d/walk_log_c5_sass_mix.txt; the price stepper
+# of the other parity configs executes 80.7): reported beside the algorithmic
+# count, it is fewer because the log-price state needs no per-step exponential.
+DP_OPS_EXECUTED_NCU = 66.3
+DP_OPS_EXECUTED_NCU_PRICE_STEPPER = 80.7
 # DRAM bytes per walker launch from the same capture (dram__bytes_read+write,
-# profiles/r01d_walk_c5_labels_pricing.txt): label launch 972.3 KB, pricing 92.4 KB
-WALK_DRAM_BYTES_PER_LAUNCH = (972.3e3 + 92.4e3) / 2
+# profiles/r02d/walk_log_c5_summary.txt): label launch 962.3 KB, pricing 80.4 KB
+WALK_DRAM_BYTES_PER_LAUNCH = (962.3e3 + 80.4e3) / 2
 FP64_LANES_PER_SM = 64
 N_SMS = 148
 # fast mode (fp32 Box-Muller) walker: issue-bound (ncu issue slots 68%, ALU
@@ -265,7 +268,9 @@ def run_engine(args, cfg):
     if mode == "fast":
         peak = ISSUE_LANES_PER_SM * N_SMS * sm_mhz * 1e6 / 1e12  # T thread-instructions/s issue peak
     ops = DP_OPS_PER_ASSET_STEP if mode == "parity" else FAST_INST_PER_ASSET_STEP
-    executed = DP_OPS_EXECUTED_NCU if mode == "parity" else FAST_INST_EXECUTED_NCU_D10
+    log_walker = cfg["method"] == "cmc" and cfg.get("payoff") == "maxcall" and not cfg.get("rho")
+    executed = ((DP_OPS_EXECUTED_NCU if log_walker else DP_OPS_EXECUTED_NCU_PRICE_STEPPER) if mode == "parity"
+                else FAST_INST_EXECUTED_NCU_D10)
     achieved = (kern_steps * cfg["d"] * ops) / (kern_ms / 1e3) / 1e12 if kern_ms > 0 else None
     total_launches = sum(v[1] for v in prof.values())
     total_kernel_ms = sum(v[0] for v in prof.values())
@@ -299,7 +304,7 @@ def run_engine(args, cfg):
                          "unit": "TFLOP/s" if mode == "parity" else "T thread-instructions/s",
                          "frac": achieved / peak if achieved is not None else None,
                          "asset_steps_per_s": kern_steps * cfg["d"] / (kern_ms / 1e3) if kern_ms > 0 else None,
-                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r01d capture)",
+                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r02d capture of the C5 walker)",
                          "kernel": "walk_units+iz_probes",
                          "work": (f"{ops:g} algorithmic " + ("fp64 ops" if mode == "parity" else "thread-instructions")
                                   + " per asset-step (SURVEY.md 8(d)) x executed asset-steps "

@@ -41,7 +41,7 @@ def _run(nproc, config, scale):
 
 
 @pytest.mark.timeout(900)
-@pytest.mark.parametrize("config,scale", [("c5", 0.03), ("c2", 0.25), ("c1", 0.25)])
+@pytest.mark.parametrize("config,scale", [("c5", 0.03), ("c2", 0.25), ("c2", 1.0), ("c1", 0.25)])
 def test_two_ranks_bitwise_equal_to_one(config, scale):
     one = _run(1, config, scale)
     two = _run(2, config, scale)

@@ -1,11 +1,13 @@
+# Round-2 (d) measurement set, run under gpurun from the repo root:
+# GPU tests, smoke, the five bench configs, the reference arm, the C5 launch list.
 set -x
-V=paper_0805_1827_b200/lib/variants
+O=gpurun_out/r02d; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-{
-timeout 600 python tools/walk_bench.py 3
-BRM_WALK_LOG=0 timeout 600 python tools/walk_bench.py 3
-for v in minb3 minb4; do BRM_LIB_PATH=$PWD/$V/libbermuda_b200_$v.so timeout 600 python tools/walk_bench.py 3; done
-} > gpurun_out/r02d_walk_bench.log 2>&1
-cat gpurun_out/r02d_walk_bench.log | grep -v "^+"
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r02d_gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r02d_gpu_tests.log
-tail -15 gpurun_out/r02d_gpu_tests.log
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "tests rc=$?" >> $O/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+timeout 900 python bench.py > $O/bench_c5.json.log 2>&1
+for c in c1 c2 c3 c4; do timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_$c.json.log 2>&1; done
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json.log 2>&1
+B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-fast-line"
+BRM_NCU_SAFE=1 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $O/launches_c5.csv $B > $O/launches_c5.log 2>&1
+tail -3 $O/gpu_tests.log
