@@ -12,7 +12,7 @@ from .boosting import Stump, StumpEnsemble, TrainingSet, fit_ensemble, fit_stump
 from .boundary_cmc import CmcBuildConfig, CmcBuildReport, CmcRule, build_cmc_rule, classifier_features
 from .boundary_iz import (BoundaryPointJob, IzBoundary, IzBuildReport, PointResult, build_iz_boundary,
                           continuation_value, regress_boundary, solve_boundary_point)
-from .engine import Engine, TaskPlan, partition
+from .engine import Engine, TaskPlan, TimingLog, partition
 from .lowdisc import SeedGrid, default_box, generate_glp, uniform_log_grid
 from .market import BermudanSpec, ConfigError, MarketParams, PayoffKind
 from .pricer import (PATH_BLOCK, CmcScoreRule, EuropeanRule, ImmediateAtDate, IzRule, PriceEstimate, pool_moments,

@@ -31,6 +31,7 @@ from . import backend as _be
 from .boosting import StumpEnsemble, ensemble_from_arrays
 from .context import get_context
 from .dist import current as _current_shard
+from .engine import log_phase, nvtx_range
 from .market import ConfigError, is_call_like
 from .packs import RulePack, pack_market
 
@@ -210,24 +211,26 @@ def _build_device_loop(params, spec, cfg, seed, sampler, mode, shard, torch, str
     for m in range(nd - 1, 0, -1):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
-        ranges = shard.local_ranges(cfg.n_train)
-        rows = sum(hi - lo for lo, hi in ranges)
-        feats = torch.empty((rows, F), dtype=f64, device="cuda")
-        betas = torch.empty((rows,), dtype=f64, device="cuda")
-        off = 0
-        for lo, hi in ranges:
-            if hi > lo:
-                _be.cmc_calc(mp, None, m, seed, lo, hi - lo, cfg.n_label, bridge_scalars(params, spec, m), sampler,
-                             feats[off:off + hi - lo], betas[off:off + hi - lo], mode=mode, ctx=ctx)
-            off += hi - lo
-        feats = shard.all_gather_rows(feats, cfg.n_train)
-        betas = shard.all_gather_rows(betas, cfg.n_train)
+        with nvtx_range(f"cmc.calc[date {m}]"):
+            ranges = shard.local_ranges(cfg.n_train)
+            rows = sum(hi - lo for lo, hi in ranges)
+            feats = torch.empty((rows, F), dtype=f64, device="cuda")
+            betas = torch.empty((rows,), dtype=f64, device="cuda")
+            off = 0
+            for lo, hi in ranges:
+                if hi > lo:
+                    _be.cmc_calc(mp, None, m, seed, lo, hi - lo, cfg.n_label, bridge_scalars(params, spec, m),
+                                 sampler, feats[off:off + hi - lo], betas[off:off + hi - lo], mode=mode, ctx=ctx)
+                off += hi - lo
+            feats = shard.all_gather_rows(feats, cfg.n_train)
+            betas = shard.all_gather_rows(betas, cfg.n_train)
         ev[1].record(stream)
-        date_out = {k: (v[m] if v.dim() == 2 else v[m:m + 1]) for k, v in out.items()}
-        date_out["n_pos"] = n_pos[m:m + 1]
-        _be.fit_ensemble_device(feats, betas, R, date_out, mode=mode, stream=stream)
-        ctx.set_ensemble(m, date_out["feat"], date_out["thr"], date_out["pol"], date_out["alpha"],
-                         date_out["count"], date_out["intercept"])
+        with nvtx_range(f"cmc.class[date {m}]"):
+            date_out = {k: (v[m] if v.dim() == 2 else v[m:m + 1]) for k, v in out.items()}
+            date_out["n_pos"] = n_pos[m:m + 1]
+            _be.fit_ensemble_device(feats, betas, R, date_out, mode=mode, stream=stream)
+            ctx.set_ensemble(m, date_out["feat"], date_out["thr"], date_out["pol"], date_out["alpha"],
+                             date_out["count"], date_out["intercept"])
         ev[2].record(stream)
         marks.append((m, ev))
     host = {k: v.cpu().numpy() for k, v in out.items()}  # the build's one synchronisation
@@ -277,7 +280,10 @@ def build_cmc_rule(params, spec, cfg: CmcBuildConfig, seed: int = 0, engine=None
     if device_loop:
         if torch is None:
             raise RuntimeError("device_loop=True needs a CUDA device")
-        return _build_device_loop(params, spec, cfg, seed, sampler, mode, shard, torch, stream, mp, F, call_like)
+        rule, report = _build_device_loop(params, spec, cfg, seed, sampler, mode, shard, torch, stream, mp, F,
+                                          call_like)
+        _log_report(engine, report)
+        return rule, report
     for m in range(spec.n_dates - 1, 0, -1):
         later = rule.pack()
         bridge = bridge_scalars(params, spec, m)
@@ -316,4 +322,11 @@ def build_cmc_rule(params, spec, cfg: CmcBuildConfig, seed: int = 0, engine=None
         report.per_date.append({"date_index": m, "calc_seconds": calc_s, "class_seconds": class_s,
                                 "positive_fraction": pos, "rounds": len(ens.rounds)})
     report.per_date.reverse()
+    _log_report(engine, report)
     return rule, report
+
+
+def _log_report(engine, report) -> None:
+    """Per-date phase times into the caller's timing log (engine.py:126-144, :167)."""
+    log_phase(engine, "calc", [(r["date_index"], r["calc_seconds"]) for r in report.per_date])
+    log_phase(engine, "class", [(r["date_index"], r["class_seconds"]) for r in report.per_date])

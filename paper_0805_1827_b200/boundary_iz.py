@@ -27,6 +27,7 @@ import numpy as np
 
 from . import backend as _be
 from .dist import current as _current_shard
+from .engine import log_phase, nvtx_range
 from .lowdisc import SeedGrid, default_box, generate_glp, uniform_log_grid
 from .market import ConfigError, is_call_like, payoff_code
 from .packs import RulePack, n_quad_basis, pack_market, quad_basis
@@ -244,18 +245,20 @@ def _build_device_loop(params, spec, n_inner, epsilon, max_iter, seed, solver, l
     for m in range(nd - 1, 0, -1):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
-        for lo, hi in shard.local_ranges(n_items):
-            if hi > lo:
-                _be.iz_solve_batch(mp, None, seeds_dev[lo:hi] if d > 1 else None, assets_dev[lo:hi], m, n_inner,
-                                   solver=solver, epsilon=epsilon, max_iter=max_iter, avg_window=5, lo=lo_b, hi=hi_b,
-                                   tol=tol, seed=seed, item_lo=lo, mode=mode, ctx=ctx,
-                                   out=(levels[m, lo:hi], iters[m, lo:hi], conv[m, lo:hi]))
-        if shard.distributed:  # disjoint rows, zero elsewhere: the sum is an exact gather
-            for t in (levels[m], iters[m], conv[m]):
-                shard.all_reduce_sum(t)
+        with nvtx_range(f"iz.calc[date {m}]"):
+            for lo, hi in shard.local_ranges(n_items):
+                if hi > lo:
+                    _be.iz_solve_batch(mp, None, seeds_dev[lo:hi] if d > 1 else None, assets_dev[lo:hi], m, n_inner,
+                                       solver=solver, epsilon=epsilon, max_iter=max_iter, avg_window=5, lo=lo_b,
+                                       hi=hi_b, tol=tol, seed=seed, item_lo=lo, mode=mode, ctx=ctx,
+                                       out=(levels[m, lo:hi], iters[m, lo:hi], conv[m, lo:hi]))
+            if shard.distributed:  # disjoint rows, zero elsewhere: the sum is an exact gather
+                for t in (levels[m], iters[m], conv[m]):
+                    shard.all_reduce_sum(t)
         ev[1].record(stream)
         # levels[m] is [n_fits * J]: fit g regresses asset g's probes (one fit in log space)
-        ctx.iz_fit(m, design, J, nb, pts.shape[1], levels[m], n_fits, iz_space == 1, coeffs[m], ranks[m])
+        with nvtx_range(f"iz.reg[date {m}]"):
+            ctx.iz_fit(m, design, J, nb, pts.shape[1], levels[m], n_fits, iz_space == 1, coeffs[m], ranks[m])
         ev[2].record(stream)
         marks.append((m, ev))
     host = {"levels": levels.cpu().numpy(), "iters": iters.cpu().numpy(), "conv": conv.cpu().numpy(),
@@ -331,9 +334,11 @@ def build_iz_boundary(params, spec, j_points: int, n_inner: int, epsilon: float 
     if device_loop:
         if torch is None:
             raise RuntimeError("device_loop=True needs a CUDA device")
-        return _build_device_loop(params, spec, n_inner, epsilon, max_iter, seed, solver, lo_b, hi_b, tol, mode,
-                                  shard, torch, mp, d, call_like, iz_space, box, reg_grid.points, assets_per_item,
-                                  item_asset, item_seed, j_points, report)
+        boundary, report = _build_device_loop(params, spec, n_inner, epsilon, max_iter, seed, solver, lo_b, hi_b, tol,
+                                              mode, shard, torch, mp, d, call_like, iz_space, box, reg_grid.points,
+                                              assets_per_item, item_asset, item_seed, j_points, report)
+        _log_report(engine, report)
+        return boundary, report
     for m in range(spec.n_dates - 1, 0, -1):
         later = boundary.pack()
         t0 = time.perf_counter()
@@ -370,4 +375,11 @@ def build_iz_boundary(params, spec, j_points: int, n_inner: int, epsilon: float 
         report.per_date.append({"date_index": m, "calc_seconds": calc_s, "reg_seconds": reg_s,
                                 "unconverged": n_unconv, "iterations": iters.tolist()})
     report.per_date.reverse()
+    _log_report(engine, report)
     return boundary, report
+
+
+def _log_report(engine, report) -> None:
+    """Per-date phase times into the caller's timing log (engine.py:126-144, :167)."""
+    log_phase(engine, "calc", [(r["date_index"], r["calc_seconds"]) for r in report.per_date])
+    log_phase(engine, "reg", [(r["date_index"], r["reg_seconds"]) for r in report.per_date])

@@ -362,6 +362,8 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   const int smem = P.vals_offset + 8 * P.chunk;
   if (smem > c->info.max_smem) return fail(BRM_EINVAL, "model image too large for shared memory (%d B)", smem);
   BRM_TRY(call.scratch<double>(2 * (size_t)P.n_items, &P.partials));
+  BRM_TRY(call.scratch<int>(1, &P.next_item));
+  BRM_CUDA(cudaMemsetAsync(P.next_item, 0, sizeof(int), call.stream));
   BRM_TRY(allow_smem(kwalk, smem));
   int per_sm = 0;
   BRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kwalk, kWalkThreads, smem));

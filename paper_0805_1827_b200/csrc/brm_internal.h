@@ -43,6 +43,7 @@ struct WalkParams {
   unsigned long long *steps;  // executed path-steps counter (may be null)
   double *path_out;  // optional [n_units * per_unit]
   int32_t *stop_out;
+  int *next_item;    // zeroed counter of claimed work items beyond the grid's first wave (null: static stride)
 };
 
 struct FinishParams {

@@ -48,7 +48,11 @@ __global__ void __launch_bounds__(kWalkThreads, SPEC == WALK_CMC_LOG ? BRM_LOG_M
   // the specialised instances never run on supplied normals (host check)
   const NormalSrc ns = SPEC == WALK_GENERIC ? NormalSrc{P.normals, P.nrm_base, P.nrm_count} : NormalSrc{nullptr, 0, 0};
 
-  for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+  // work items are claimed from a counter (the first one is the CTA's own
+  // index): items differ in length with their unit's moneyness, and a static
+  // stride leaves the last CTAs ~3 sigma of an item-sum behind the mean
+  __shared__ int s_item;
+  for (int item = blockIdx.x; item < P.n_items; item = s_item) {
     const int u = item / P.chunks_per_unit;
     const int c = item - u * P.chunks_per_unit;
     const int64_t cnt64 = P.total_paths - (int64_t)u * P.per_unit;
@@ -62,7 +66,6 @@ __global__ void __launch_bounds__(kWalkThreads, SPEC == WALK_CMC_LOG ? BRM_LOG_M
     } else {
       derive_words(P.seed, (uint64_t)P.phase, (uint64_t)(P.item_base + u), (uint64_t)P.key_date, key, stream);
     }
-    __syncthreads();  // previous item finished with s_start / vals / s_next
     if (threadIdx.x < d) {
       const R s = P.starts ? (R)P.starts[(size_t)u * P.start_stride + threadIdx.x] : M.s0[threadIdx.x];
       if constexpr (kLog) s_start[threadIdx.x] = log(s);
@@ -89,7 +92,9 @@ __global__ void __launch_bounds__(kWalkThreads, SPEC == WALK_CMC_LOG ? BRM_LOG_M
     if (threadIdx.x == 0) {
       P.partials[2 * (size_t)item] = s;
       P.partials[2 * (size_t)item + 1] = q;
+      s_item = P.next_item ? (int)gridDim.x + atomicAdd(P.next_item, 1) : item + (int)gridDim.x;
     }
+    __syncthreads();  // the next item is known, and this one is finished with s_start / vals / s_next
   }
 }
 

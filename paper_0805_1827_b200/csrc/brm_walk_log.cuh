@@ -58,6 +58,14 @@ __device__ __forceinline__ double lds_f64(unsigned addr) {
   return v;
 }
 
+// One level of a search tree: a <- 2 a + k + 8 [t < x] (k = 8 - tree base),
+// the comparison as a predicated add (three instructions with the load).
+__device__ __forceinline__ unsigned tree_step(unsigned a, unsigned k, double t, double x) {
+  unsigned na = 2u * a + k;
+  asm("{ .reg .pred p; setp.lt.f64 p, %1, %2; @p add.u32 %0, %0, 8; }" : "+r"(na) : "d"(t), "d"(x));
+  return na;
+}
+
 // Stump score through the per-feature search trees (build_log_tables): D + 1
 // branch-free searches in lock-step, then a pairwise sum.  The sum is in a
 // different order than the reference's, so it decides only outside the
@@ -81,7 +89,7 @@ __device__ __forceinline__ bool cmc_stop_log(const Model<double> &M, int m, cons
 #pragma unroll
     for (int f = 0; f < FN; ++f) t[f] = lds_f64(a[f]);
 #pragma unroll
-    for (int f = 0; f < FN; ++f) a[f] = 2u * a[f] + kf[f] + (t[f] < (f < D ? x[f < D ? f : 0] : xmax) ? 8u : 0u);
+    for (int f = 0; f < FN; ++f) a[f] = tree_step(a[f], kf[f], t[f], f < D ? x[f < D ? f : 0] : xmax);
   }
 #pragma unroll 1
   for (int l = dmin; l < M.lt_d1; ++l) {  // deeper asset trees
@@ -89,11 +97,11 @@ __device__ __forceinline__ bool cmc_stop_log(const Model<double> &M, int m, cons
 #pragma unroll
     for (int f = 0; f < D; ++f) t[f] = lds_f64(a[f]);
 #pragma unroll
-    for (int f = 0; f < D; ++f) a[f] = 2u * a[f] + kf[f] + (t[f] < x[f] ? 8u : 0u);
+    for (int f = 0; f < D; ++f) a[f] = tree_step(a[f], kf[f], t[f], x[f]);
   }
 #pragma unroll 1
   for (int l = dmin; l < M.lt_d2; ++l)  // deeper derived-feature tree
-    a[D] = 2u * a[D] + kf[D] + (lds_f64(a[D]) < xmax ? 8u : 0u);
+    a[D] = tree_step(a[D], kf[D], lds_f64(a[D]), xmax);
   double val[FN];
 #pragma unroll
   for (int f = 0; f < FN; ++f) val[f] = lds_f64(a[f]);

@@ -17,6 +17,7 @@ import numpy as np
 
 from . import backend as _be
 from .dist import current as _current_shard
+from .engine import log_phase, nvtx_range
 from .packs import RulePack, pack_market
 
 __all__ = ["PATH_BLOCK", "EuropeanRule", "ImmediateAtDate", "IzRule", "CmcScoreRule", "PriceEstimate", "price",
@@ -135,8 +136,10 @@ def price(params, spec, rule, n_paths: int, seed: int, engine=None, backend=None
     mp = pack_market(params, spec)
     rp = rule.pack(spec)
     t0 = time.perf_counter()
-    stats = block_stats(mp, rp, n_paths, seed, mode=mode)
+    with nvtx_range("mc"):
+        stats = block_stats(mp, rp, n_paths, seed, mode=mode)
     pricing_seconds = time.perf_counter() - t0
+    log_phase(engine, "mc", [(_current_shard().rank, pricing_seconds)])
     mean, var, n = pool_moments(stats[:, 0], stats[:, 1], stats[:, 2])
     timings = dict(build_timings or {})
     timings["pricing"] = pricing_seconds

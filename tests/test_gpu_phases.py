@@ -135,3 +135,22 @@ def test_put_1d_bisection_near_lattice():
     est = E.price(pe, se, E.IzRule(b), 1 << 18, 1827, mode="parity")
     exact = O.crr_bermudan(40.0, 40.0, 0.06, 0.0, 0.2, 1.0, 10, 5000, put=True)
     assert abs(est.price - exact) < 4 * est.std_error + 0.01
+
+
+def test_builders_fill_the_engine_timing_log():
+    """Per-date device times land in the caller's engine.timing (engine.py:126-144, :167) under the
+    reference's phase names, for both builders and the pricer."""
+    from tests import _cases as CS
+    eng = E.Engine(workers=1)
+    p, s = CS.maxcall(3, n_dates=4)
+    rule, rep = E.build_cmc_rule(p, s, E.CmcBuildConfig(300, 64, 10), seed=3, engine=eng)
+    est = E.price(p, s, E.CmcScoreRule(rule), 1 << 14, 3, engine=eng)
+    phases = [r[0] for r in eng.timing.rows]
+    assert phases.count("calc") == 3 and phases.count("class") == 3 and phases.count("mc") == 1
+    assert abs(eng.timing.phase_seconds("calc") - rep.calc_seconds) < 1e-9
+    assert eng.timing.straggler_ratio("calc") >= 1.0
+    assert est.timings["pricing"] > 0.0
+    p1, s1 = CS.put1d(n_dates=4)
+    eng2 = E.Engine(workers=1)
+    E.build_iz_boundary(p1, s1, 8, 256, seed=2, engine=eng2)
+    assert [r[0] for r in eng2.timing.rows].count("reg") == 3

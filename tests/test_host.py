@@ -93,3 +93,24 @@ def test_bench_nominal_work_and_sample():
     assert bench.nominal_path_steps(c1) == 1 * 18 * 2000 * 45 + (1 << 18) * 10
     s = bench.reference_sample(c5)
     assert s["n_label"] == c5["n_label"] and s["n_train"] < c5["n_train"]
+
+
+def test_timing_log_matches_reference_semantics():
+    """TimingLog (engine.py:126-144): phase totals and the max / median straggler ratio."""
+    from paper_0805_1827_b200.engine import Engine, TimingLog, log_phase
+    log = TimingLog()
+    assert log.straggler_ratio("calc") == 1.0 and log.phase_seconds("calc") == 0.0
+    eng = Engine(workers=1)
+    log_phase(eng, "calc", [(8, 0.5), (7, 1.5), (6, 1.0)])
+    log_phase(eng, "class", [(8, 0.0)])
+    log_phase(None, "calc", [(1, 1.0)])  # no engine, no log: ignored
+    assert eng.timing.rows[:2] == [("calc", 8, 0.5), ("calc", 7, 1.5)]
+    assert eng.timing.phase_seconds("calc") == 3.0
+    assert eng.timing.straggler_ratio("calc") == 1.5
+    assert eng.timing.straggler_ratio("class") == 1.0  # zero median
+
+
+def test_nvtx_range_is_a_noop_without_cuda():
+    from paper_0805_1827_b200.engine import nvtx_range
+    with nvtx_range("phase"):
+        pass
