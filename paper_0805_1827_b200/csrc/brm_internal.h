@@ -11,7 +11,7 @@ namespace brm {
 
 constexpr int kWalkThreads = 256;   // threads per walker CTA
 constexpr int kPathBlock = 4096;    // pricer.py:32 PATH_BLOCK (stream convention)
-constexpr int kPriceChunk = 1024;   // paths per pricing work item (4 per block)
+constexpr int kPriceChunk = 2048;   // paths per pricing work item (2 per block: 8 paths per lane before the drain)
 constexpr int kMaxChunk = 2048;     // largest chunk a walker CTA folds in smem
 constexpr int kIzFoldChunk = 256;   // I&Z probes: paths per fixed-order fold chunk
 constexpr int kIzMaxChunks = 64;    // fold chunks per probe CTA (16384 inner paths)
