@@ -58,14 +58,14 @@ CONFIGS = {
 DP_OPS_PER_ASSET_STEP = 70.0
 # What the walker actually executes on the fp64 pipe (ncu: DADD+DMUL+DFMA+DSETP
 # thread instructions / executed asset-steps on the C5 label launch of the
-# log-price walker, profiles/r02d/walk_log_c5_sass_mix.txt; the price stepper
+# log-price walker, profiles/r02e/walk_log_c5_sass_mix.txt; the price stepper
 # of the other parity configs executes 80.7): reported beside the algorithmic
 # count, it is fewer because the log-price state needs no per-step exponential.
 DP_OPS_EXECUTED_NCU = 66.3
 DP_OPS_EXECUTED_NCU_PRICE_STEPPER = 80.7
 # DRAM bytes per walker launch from the same capture (dram__bytes_read+write,
-# profiles/r02d/walk_log_c5_summary.txt): label launch 962.3 KB, pricing 80.4 KB
-WALK_DRAM_BYTES_PER_LAUNCH = (962.3e3 + 80.4e3) / 2
+# profiles/r02e/walk_log_c5_summary.txt): label launch 959.7 KB, pricing 80.4 KB
+WALK_DRAM_BYTES_PER_LAUNCH = (959.7e3 + 80.4e3) / 2
 FP64_LANES_PER_SM = 64
 N_SMS = 148
 # fast mode (fp32 Box-Muller) walker: issue-bound (ncu issue slots 68%, ALU
@@ -304,7 +304,7 @@ def run_engine(args, cfg):
                          "unit": "TFLOP/s" if mode == "parity" else "T thread-instructions/s",
                          "frac": achieved / peak if achieved is not None else None,
                          "asset_steps_per_s": kern_steps * cfg["d"] / (kern_ms / 1e3) if kern_ms > 0 else None,
-                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r02d capture of the C5 walker)",
+                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r02e capture of the C5 walker)",
                          "kernel": "walk_units+iz_probes",
                          "work": (f"{ops:g} algorithmic " + ("fp64 ops" if mode == "parity" else "thread-instructions")
                                   + " per asset-step (SURVEY.md 8(d)) x executed asset-steps "

@@ -110,7 +110,8 @@ def fit_stump(xs, ys, weights, mode=None) -> tuple[Stump, float]:
 
 
 def ensemble_from_arrays(dim, feat, thr, pol, alpha, intercept) -> StumpEnsemble:
-    rounds = tuple(Stump(int(f), float(t), float(p), float(a)) for f, t, p, a in zip(feat, thr, pol, alpha))
+    cols = [np.asarray(c).tolist() for c in (feat, thr, pol, alpha)]  # Python scalars in one pass per column
+    rounds = tuple(Stump(int(f), float(t), float(p), float(a)) for f, t, p, a in zip(*cols))
     return StumpEnsemble(dim=int(dim), rounds=rounds, intercept=float(intercept))
 
 

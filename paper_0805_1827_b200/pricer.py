@@ -91,10 +91,10 @@ class PriceEstimate:
 def pool_moments(counts, sums, sumsqs) -> tuple[float, float, int]:
     """Fold per-block (count, sum, sumsq) in block order (pricer.py:136-151)."""
     n = int(np.sum(counts))
-    s = ss = 0.0
-    for si, qi in zip(sums, sumsqs):
-        s += float(si)
-        ss += float(qi)
+    # numpy's cumsum is the sequential chain ((x0 + x1) + x2) + ...: the same fp64 adds, in block
+    # order, as the reference's Python loop (unlike np.sum, which adds pairwise)
+    s = float(np.cumsum(np.asarray(sums, dtype=np.float64))[-1]) if len(sums) else 0.0
+    ss = float(np.cumsum(np.asarray(sumsqs, dtype=np.float64))[-1]) if len(sumsqs) else 0.0
     mean = s / n
     var = (ss - s * s / n) / (n - 1) if n > 1 else 0.0
     return mean, max(var, 0.0), n
