@@ -1244,6 +1244,14 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   const int smem = P.hist_offset + 8 * (P.max_iter + 1);
   if (smem > c->info.max_smem) return fail(BRM_EINVAL, "probe solve needs %d B of shared memory", smem);
   void *kiz = (c->hdr.payoff == BRM_PAY_GEOPUT && !c->fast() && c->kern.iz_geo) ? c->kern.iz_geo : c->kern.iz;
+  {
+    // parity mode walks log-prices when the rule is the geometric put's log-space surface over
+    // independent assets (brm_walk_log.cuh); BRM_WALK_LOG=0 keeps the price stepper (A/B runs)
+    static const bool log_walk = !(std::getenv("BRM_WALK_LOG") && std::getenv("BRM_WALK_LOG")[0] == '0');
+    if (log_walk && c->hdr.payoff == BRM_PAY_GEOPUT && !c->fast() && c->hdr.rule == BRM_RULE_IZ &&
+        c->hdr.iz_space == 1 && c->hdr.unit_diag && !P.normals && c->kern.iz_geo_log)
+      kiz = c->kern.iz_geo_log;
+  }
   BRM_TRY(allow_smem(kiz, smem));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(n * csize));

@@ -108,6 +108,7 @@ struct KernelTriple {
   void *walk_cmc_unit = nullptr;  // ... max-call payoff, independent assets (unit diagonal factor)
   void *walk_cmc_lower = nullptr; // ... fast mode, lower-triangular factor
   void *walk_cmc_log = nullptr;   // ... walk_cmc_unit's case in parity mode on log-prices (brm_walk_log.cuh)
+  void *iz_geo_log = nullptr;     // iz_geo on log-prices (log-space surface, independent assets; brm_walk_log.cuh)
 };
 
 // Kernel families for launch accounting (brm_prof.cu, BRM_PROF_* in the C ABI).

@@ -8,8 +8,8 @@ KernelTriple kernels_d10(bool fast) {
                         nullptr, (void *)&walk_units<10, true, WALK_CMC>,
                         (void *)&walk_units<10, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<10, false>, (void *)&iz_probes<10, false>, (void *)&decisions<10, false>,
-                      (void *)&iz_probes<10, false, true>, (void *)&walk_units<10, false, WALK_CMC>,
+                      (void *)&iz_probes<10, false, 1>, (void *)&walk_units<10, false, WALK_CMC>,
                       (void *)&walk_units<10, false, WALK_CMC_UNIT>, nullptr,
-                      (void *)&walk_units<10, false, WALK_CMC_LOG>};
+                      (void *)&walk_units<10, false, WALK_CMC_LOG>, (void *)&iz_probes<10, false, 2>};
 }
 }  // namespace brm

@@ -8,8 +8,8 @@ KernelTriple kernels_d3(bool fast) {
                         nullptr, (void *)&walk_units<3, true, WALK_CMC>,
                         (void *)&walk_units<3, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<3, false>, (void *)&iz_probes<3, false>, (void *)&decisions<3, false>,
-                      (void *)&iz_probes<3, false, true>, (void *)&walk_units<3, false, WALK_CMC>,
+                      (void *)&iz_probes<3, false, 1>, (void *)&walk_units<3, false, WALK_CMC>,
                       (void *)&walk_units<3, false, WALK_CMC_UNIT>, nullptr,
-                      (void *)&walk_units<3, false, WALK_CMC_LOG>};
+                      (void *)&walk_units<3, false, WALK_CMC_LOG>, (void *)&iz_probes<3, false, 2>};
 }
 }  // namespace brm

@@ -8,8 +8,8 @@ KernelTriple kernels_d5(bool fast) {
                         nullptr, (void *)&walk_units<5, true, WALK_CMC>,
                         (void *)&walk_units<5, true, WALK_CMC_UNIT>};
   return KernelTriple{(void *)&walk_units<5, false>, (void *)&iz_probes<5, false>, (void *)&decisions<5, false>,
-                      (void *)&iz_probes<5, false, true>, (void *)&walk_units<5, false, WALK_CMC>,
+                      (void *)&iz_probes<5, false, 1>, (void *)&walk_units<5, false, WALK_CMC>,
                       (void *)&walk_units<5, false, WALK_CMC_UNIT>, nullptr,
-                      (void *)&walk_units<5, false, WALK_CMC_LOG>};
+                      (void *)&walk_units<5, false, WALK_CMC_LOG>, (void *)&iz_probes<5, false, 2>};
 }
 }  // namespace brm

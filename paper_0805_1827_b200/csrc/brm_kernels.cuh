@@ -144,10 +144,13 @@ __device__ __forceinline__ void fold_chunks(const double *vals, int n, double *s
   __syncthreads();
 }
 
-// GEOK: the geometric-put instance (walk_paths' GEO step; launched only for
-// that payoff).
-template <int D, bool FAST, bool GEOK = false>
+// GEOK 1: the geometric-put instance (walk_paths' GEO step; launched only for
+// that payoff).  GEOK 2: the geometric put on log-prices (walk_paths_log's
+// LOG_GEOPUT_IZ; parity mode, log-space I&Z surface, independent assets).
+template <int D, bool FAST, int GEOK = 0>
 __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
+  static_assert(GEOK != 2 || (!FAST && D > 1), "the log-price probe walker is a parity instance for d > 1");
+  [[maybe_unused]] const double log_strike = GEOK == 2 ? log(P.hdr.strike) : 0.0;
   constexpr int TG = FAST ? 1 : TailGroup<D>::G;
   __shared__ double s_tq_buf[(kWalkThreads / 32) * 32 * TG];
   __shared__ unsigned short s_tq_idx[(kWalkThreads / 32) * 32 * TG];
@@ -237,13 +240,18 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
         const double x = *x_remote;
         if (threadIdx.x == 0) probe_state(P.hdr, seedp, asset, x, s_state);
         __syncthreads();
-        if (threadIdx.x < d) s_start[threadIdx.x] = (R)s_state[threadIdx.x];
+        if (threadIdx.x < d) s_start[threadIdx.x] = GEOK == 2 ? (R)log(s_state[threadIdx.x]) : (R)s_state[threadIdx.x];
         if (threadIdx.x == 0) s_next = p0 + blockDim.x;
         __syncthreads();
         const uint64_t base0 = unit_base<FAST>(0, P.normals != nullptr);
-        if (p0 < p1)
-          walk_paths<D, FAST, GEOK ? WALK_GEO : WALK_GENERIC>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1,
-                                                              ns, vals, &s_next, nullptr, nullptr, P.steps, tq);
+        if (p0 < p1) {
+          if constexpr (GEOK == 2)
+            walk_paths_log<(D > 1 ? D : 2), LOG_GEOPUT_IZ>(M, s_start, log_strike, P.m, P.n_steps, key, stream, base0,
+                                                           p0, p1, vals, nullptr, &s_next, P.steps, tq);
+          else
+            walk_paths<D, FAST, GEOK ? WALK_GEO : WALK_GENERIC>(M, s_start, P.m, P.n_steps, key, stream, base0, p0,
+                                                                p1, ns, vals, &s_next, nullptr, nullptr, P.steps, tq);
+        }
         __syncthreads();
         fold_chunks(vals, p1 > p0 ? p1 - p0 : 0, s_chunk);
       }
@@ -304,16 +312,20 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
     const double x = *x_remote;
     if (threadIdx.x == 0) probe_state(P.hdr, seedp, asset, x, s_state);
     __syncthreads();
-    if (threadIdx.x < d) s_start[threadIdx.x] = (R)s_state[threadIdx.x];
+    if (threadIdx.x < d) s_start[threadIdx.x] = GEOK == 2 ? (R)log(s_state[threadIdx.x]) : (R)s_state[threadIdx.x];
     if (threadIdx.x == 0) s_next = p0 + blockDim.x;
     __syncthreads();
     // fixed point: fresh slab per iteration; bisection: common random numbers
     const uint64_t draw_base = P.solver == 0 ? (uint64_t)it * slab : 0;
     const uint64_t base0 = unit_base<FAST>(draw_base, P.normals != nullptr);
-    if (p0 < p1)
-      walk_paths<D, FAST, GEOK ? WALK_GEO : WALK_GENERIC>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1, ns,
-                                                          vals, &s_next, nullptr,
-                          nullptr, P.steps, tq);
+    if (p0 < p1) {
+      if constexpr (GEOK == 2)
+        walk_paths_log<(D > 1 ? D : 2), LOG_GEOPUT_IZ>(M, s_start, log_strike, P.m, P.n_steps, key, stream, base0, p0,
+                                                       p1, vals, nullptr, &s_next, P.steps, tq);
+      else
+        walk_paths<D, FAST, GEOK ? WALK_GEO : WALK_GENERIC>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1,
+                                                            ns, vals, &s_next, nullptr, nullptr, P.steps, tq);
+    }
     __syncthreads();
     // fixed-order fold in 256-path chunks: the chunk sums are added in path
     // order by rank 0, so the continuation value does not depend on the

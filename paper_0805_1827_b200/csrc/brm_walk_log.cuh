@@ -1,5 +1,8 @@
-// brm_walk_log.cuh -- the log-price walker instance (WALK_CMC_LOG): max-call
-// payoff, CMC rule, independent assets, parity draws (C3 / C5 in fp64).
+// brm_walk_log.cuh -- the log-price walker instances, parity draws in fp64:
+//   LOG_MAXCALL_CMC  max-call payoff, CMC rule, independent assets (C3 / C5;
+//                    walk_units<.., WALK_CMC_LOG>)
+//   LOG_GEOPUT_IZ    geometric-average put, I&Z log-space surface, independent
+//                    assets (the probe clusters of C2; iz_probes<.., 2>)
 //
 // The reference's _path_value (_core.pyx:290-323) steps prices,
 // v_i <- v_i * exp(mu_i + vol_i z_i), and needs d exponentials per step.  For
@@ -29,6 +32,11 @@
 // payoff (exp(x_max) - K) disc is formed afterwards by all lanes of the CTA
 // (finish_log_values) instead of by the two or three lanes of a warp that
 // stop in a given step.
+//
+// The geometric put needs even less: its payoff K - exp(mean_i x_i) and its
+// log-space boundary surface (x_d against a quadratic in the other x_j) are
+// functions of the log-prices, so the price stepper's d exponentials and d
+// logarithms per step become one exponential per stopped path.
 #pragma once
 #include "brm_walk.cuh"
 
@@ -182,16 +190,32 @@ __device__ __forceinline__ void step_log_prices(const Model<double> &M, const Ph
   }
 }
 
-// Walk paths [p0, p1) of one unit from the shared start log-prices x_start
-// (lane refill as walk_paths, brm_walk.cuh).  Slot p - p0 of vals receives the
-// stopped path's x_max and stopm its stop date (0: expired worthless);
-// finish_log_values turns them into discounted payoffs.
+enum { LOG_MAXCALL_CMC = 0, LOG_GEOPUT_IZ = 1 };
+
+// Log-space boundary decision of the geometric put (iz_stop's iz_space == 1
+// branch, brm_model.cuh, on the state's own log-prices).
 template <int D>
+__device__ __forceinline__ bool iz_stop_log(const Model<double> &M, int m, const double *x) {
+  constexpr int k = D - 1;
+  double w[k];
+#pragma unroll
+  for (int j = 0; j < k; ++j) w[j] = x[j] < M.izlo[j] ? M.izlo[j] : (x[j] > M.izhi[j] ? M.izhi[j] : x[j]);
+  const double *row = M.izc + ((size_t)m * D + (D - 1)) * M.nbasis;
+  return x[D - 1] <= quad_surface<D>(row, w, k);
+}
+
+// Walk paths [p0, p1) of one unit from the shared start log-prices x_start
+// (lane refill as walk_paths, brm_walk.cuh).
+// LOG_MAXCALL_CMC: slot p - p0 of vals receives the stopped path's x_max and
+// stopm its stop date (0: expired worthless); finish_log_values turns them
+// into discounted payoffs.  LOG_GEOPUT_IZ: vals receives the discounted payoff
+// itself (stopm unused; the probe clusters fold vals as they are).
+template <int D, int KIND = LOG_MAXCALL_CMC>
 __device__ void walk_paths_log(const Model<double> &M, const double *x_start, double log_strike, int m_start,
                                int n_steps, uint64_t key, uint64_t stream, uint64_t base0, int p0, int p1,
                                double *vals, unsigned char *stopm, int *s_next, unsigned long long *step_count,
                                const TailQueue &tq) {
-  static_assert(D > 1, "the log-price walker is the d > 1 max-call instance");
+  static_assert(D > 1, "the log-price walkers are d > 1 instances");
   const uint64_t stride = (uint64_t)n_steps * (uint64_t)D;
   const unsigned lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -216,15 +240,30 @@ __device__ void walk_paths_log(const Model<double> &M, const double *x_start, do
     if (have) {
       ++nsteps;
       const int m = m_start + k + 1;
-      double xmax = x[0];
+      bool stop;
+      if constexpr (KIND == LOG_GEOPUT_IZ) {
+        // geometric mean in log space: the same sequential sum and divide as geo_payoff (brm_walk.cuh)
+        double sx = 0.0;
 #pragma unroll
-      for (int i = 1; i < D; ++i)
-        if (x[i] > xmax) xmax = x[i];
-      const double dk = r_sub(xmax, log_strike);
-      bool itm = dk > 0.0;
-      if (fabs(dk) <= 1e-13) itm = r_sub(exp_nb(xmax), M.strike) > 0.0;  // decide at the money in price space
-      if (itm && (m == M.n_dates || cmc_stop_log<D>(M, m, x, xmax))) {
-        xstop = xmax;
+        for (int i = 0; i < D; ++i) sx = r_add(sx, x[i]);
+        const double g = __ddiv_rn(sx, (double)D);
+        const double dk = r_sub(log_strike, g);
+        bool itm = dk > 0.0;
+        if (fabs(dk) <= 1e-13) itm = r_sub(M.strike, exp_nb(g)) > 0.0;  // decide at the money in price space
+        stop = itm && (m == M.n_dates || iz_stop_log<D>(M, m, x));
+        if (stop) xstop = r_mul(r_sub(M.strike, exp_nb(g)), M.disc[m - m_start]);
+      } else {
+        double xmax = x[0];
+#pragma unroll
+        for (int i = 1; i < D; ++i)
+          if (x[i] > xmax) xmax = x[i];
+        const double dk = r_sub(xmax, log_strike);
+        bool itm = dk > 0.0;
+        if (fabs(dk) <= 1e-13) itm = r_sub(exp_nb(xmax), M.strike) > 0.0;  // decide at the money in price space
+        stop = itm && (m == M.n_dates || cmc_stop_log<D>(M, m, x, xmax));
+        if (stop) xstop = xmax;
+      }
+      if (stop) {
         stop_m = m;
         done = true;
       } else if (k + 1 == n_steps) {
@@ -235,7 +274,7 @@ __device__ void walk_paths_log(const Model<double> &M, const double *x_start, do
     }
     if (done) {
       vals[p - p0] = xstop;
-      stopm[p - p0] = (unsigned char)stop_m;
+      if constexpr (KIND == LOG_MAXCALL_CMC) stopm[p - p0] = (unsigned char)stop_m;
     }
     const unsigned need = __ballot_sync(0xffffffffu, done);
     if (need) {
