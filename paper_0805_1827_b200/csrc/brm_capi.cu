@@ -1295,6 +1295,19 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
       cfg.numAttrs = 1;
     }
   }
+  // draw cache of the sequential bisection on the log-price walker: every pass walks the same
+  // paths (common random numbers), so the first one records the increments and the rest replay
+  // them from HBM (C2: 115 MB per date); BRM_IZ_NO_CACHE=1 re-simulates every pass (A/B runs)
+  P.rec = nullptr;
+  if (solver == 1 && P.tree_levels == 1 && kiz == c->kern.iz_geo_log && c->kern.iz_geo_log_rec && P.max_iter > 1 &&
+      getenv("BRM_IZ_NO_CACHE") == nullptr) {
+    const size_t cells = (size_t)n * P.n_steps * n_inner * c->hdr.d;
+    if (cells <= ((size_t)1 << 28)) {  // <= 2 GB
+      BRM_TRY(call.scratch<double>(cells, &P.rec));
+      kiz = c->kern.iz_geo_log_rec;  // same launch shape and shared memory
+      BRM_TRY(allow_smem(kiz, smem));
+    }
+  }
   void *args[] = {&P};
   {
     const int tok_ = prof_begin(PK_IZ, call.stream);

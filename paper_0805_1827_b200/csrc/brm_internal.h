@@ -81,6 +81,10 @@ struct IzParams {
   // per pass on as many clusters (cooperative launch), tree_passes passes
   int tree_levels, tree_passes;
   double *tree_cont;  // [2][n_probes][2^L - 1] node continuation values
+  // bisection draw cache (log-price probe walker, sequential bisection): the
+  // first pass records every path's increments, [n_probes][n_steps][n_inner][d];
+  // the later passes replay them (null: every pass re-simulates)
+  double *rec;
 };
 
 struct DecisionParams {
@@ -109,6 +113,7 @@ struct KernelTriple {
   void *walk_cmc_lower = nullptr; // ... fast mode, lower-triangular factor
   void *walk_cmc_log = nullptr;   // ... walk_cmc_unit's case in parity mode on log-prices (brm_walk_log.cuh)
   void *iz_geo_log = nullptr;     // iz_geo on log-prices (log-space surface, independent assets; brm_walk_log.cuh)
+  void *iz_geo_log_rec = nullptr; // ... with the bisection draw cache (first pass records, the others replay)
 };
 
 // Kernel families for launch accounting (brm_prof.cu, BRM_PROF_* in the C ABI).

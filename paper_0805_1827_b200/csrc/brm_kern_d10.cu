@@ -10,6 +10,7 @@ KernelTriple kernels_d10(bool fast) {
   return KernelTriple{(void *)&walk_units<10, false>, (void *)&iz_probes<10, false>, (void *)&decisions<10, false>,
                       (void *)&iz_probes<10, false, 1>, (void *)&walk_units<10, false, WALK_CMC>,
                       (void *)&walk_units<10, false, WALK_CMC_UNIT>, nullptr,
-                      (void *)&walk_units<10, false, WALK_CMC_LOG>, (void *)&iz_probes<10, false, 2>};
+                      (void *)&walk_units<10, false, WALK_CMC_LOG>, (void *)&iz_probes<10, false, 2>,
+                      (void *)&iz_probes<10, false, 3>};
 }
 }  // namespace brm

@@ -10,6 +10,7 @@ KernelTriple kernels_d2(bool fast) {
   return KernelTriple{(void *)&walk_units<2, false>, (void *)&iz_probes<2, false>, (void *)&decisions<2, false>,
                       (void *)&iz_probes<2, false, 1>, (void *)&walk_units<2, false, WALK_CMC>,
                       (void *)&walk_units<2, false, WALK_CMC_UNIT>, nullptr,
-                      (void *)&walk_units<2, false, WALK_CMC_LOG>, (void *)&iz_probes<2, false, 2>};
+                      (void *)&walk_units<2, false, WALK_CMC_LOG>, (void *)&iz_probes<2, false, 2>,
+                      (void *)&iz_probes<2, false, 3>};
 }
 }  // namespace brm

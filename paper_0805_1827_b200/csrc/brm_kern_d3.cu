@@ -10,6 +10,7 @@ KernelTriple kernels_d3(bool fast) {
   return KernelTriple{(void *)&walk_units<3, false>, (void *)&iz_probes<3, false>, (void *)&decisions<3, false>,
                       (void *)&iz_probes<3, false, 1>, (void *)&walk_units<3, false, WALK_CMC>,
                       (void *)&walk_units<3, false, WALK_CMC_UNIT>, nullptr,
-                      (void *)&walk_units<3, false, WALK_CMC_LOG>, (void *)&iz_probes<3, false, 2>};
+                      (void *)&walk_units<3, false, WALK_CMC_LOG>, (void *)&iz_probes<3, false, 2>,
+                      (void *)&iz_probes<3, false, 3>};
 }
 }  // namespace brm

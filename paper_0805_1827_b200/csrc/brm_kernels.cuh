@@ -144,11 +144,31 @@ __device__ __forceinline__ void fold_chunks(const double *vals, int n, double *s
   __syncthreads();
 }
 
-// GEOK 1: the geometric-put instance (walk_paths' GEO step; launched only for
-// that payoff).  GEOK 2: the geometric put on log-prices (walk_paths_log's
+// Rank 0 of a probe cluster: the chunk sums of every CTA of the cluster, fetched
+// over distributed shared memory by the lanes of warp 0 in parallel (one
+// thread fetching them one after the other pays a remote round trip per
+// chunk), into s_all in path order.  The caller's thread 0 then adds them in
+// that order, so the sum does not depend on the cluster size.  Warp 0 only.
+__device__ __forceinline__ int gather_chunk_sums(cg::cluster_group &cluster, double *s_chunk, int csize, int per_cta,
+                                                 int n_inner, double *s_all) {
+  const int per_cta_chunks = per_cta / kIzFoldChunk;
+  const int n_chunks = (n_inner + kIzFoldChunk - 1) / kIzFoldChunk;
+  for (int g = threadIdx.x; g < n_chunks; g += 32) {
+    const int r = g / per_cta_chunks;
+    s_all[g] = cluster.map_shared_rank(s_chunk, r)[g - r * per_cta_chunks];
+  }
+  __syncwarp();
+  return n_chunks;
+}
+
+// GMODE 1: the geometric-put instance (walk_paths' GEO step; launched only for
+// that payoff).  GMODE 2: the geometric put on log-prices (walk_paths_log's
 // LOG_GEOPUT_IZ; parity mode, log-space I&Z surface, independent assets).
-template <int D, bool FAST, int GEOK = 0>
+// GMODE 3: GMODE 2 with the bisection draw cache (P.rec): the first pass
+// records the paths' increments, the others replay them.
+template <int D, bool FAST, int GMODE = 0>
 __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
+  constexpr int GEOK = GMODE == 3 ? 2 : GMODE;
   static_assert(GEOK != 2 || (!FAST && D > 1), "the log-price probe walker is a parity instance for d > 1");
   [[maybe_unused]] const double log_strike = GEOK == 2 ? log(P.hdr.strike) : 0.0;
   constexpr int TG = FAST ? 1 : TailGroup<D>::G;
@@ -169,6 +189,7 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
   __shared__ R s_start[kMaxD];
   __shared__ double s_state[kMaxD];
   __shared__ double s_chunk[kIzMaxChunks];  // this CTA's 256-path chunk sums
+  __shared__ double s_all[kIzMaxChunks * 8];  // rank 0: every CTA's chunk sums in path order
   __shared__ double s_x, s_lo, s_hi;        // rank 0: solver state
   __shared__ int s_done, s_it, s_armed, s_conv;
   const Model<R> M = load_model<R>(P.hdr, P.blob, smem);
@@ -257,14 +278,13 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
       }
       cluster.sync();
       double *cont_buf = P.tree_cont + (size_t)(pass & 1) * P.n_probes * kt + (size_t)probe * kt;
-      if (rank == 0 && threadIdx.x == 0 && !done) {
-        double total = 0.0;
-        for (int r = 0; r < csize; ++r) {
-          const double *rc = cluster.map_shared_rank(s_chunk, r);
-          for (int c = 0; r * per_cta + c * kIzFoldChunk < min((r + 1) * per_cta, P.n_inner); ++c)
-            total = __dadd_rn(total, rc[c]);
+      if (rank == 0 && threadIdx.x < 32 && !done) {
+        const int n_chunks = gather_chunk_sums(cluster, s_chunk, csize, per_cta, P.n_inner, s_all);
+        if (threadIdx.x == 0) {
+          double total = 0.0;
+          for (int g = 0; g < n_chunks; ++g) total = __dadd_rn(total, s_all[g]);
+          cont_buf[slot] = __ddiv_rn(total, (double)P.n_inner);
         }
-        cont_buf[slot] = __ddiv_rn(total, (double)P.n_inner);
       }
       grid.sync();  // (double-buffered by pass: a cluster may publish pass p+1 while another reads pass p)
       if (rank == 0 && threadIdx.x == 0 && !s_done) {
@@ -319,12 +339,24 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
     const uint64_t draw_base = P.solver == 0 ? (uint64_t)it * slab : 0;
     const uint64_t base0 = unit_base<FAST>(draw_base, P.normals != nullptr);
     if (p0 < p1) {
-      if constexpr (GEOK == 2)
+      if constexpr (GMODE == 3) {
+        // bisection walks the same paths every pass (common random numbers): the first pass
+        // records their increments and the others replay them
+        constexpr int DL = D > 1 ? D : 2;
+        double *rec = P.rec + (size_t)probe * P.n_steps * P.n_inner * d;
+        if (it > 0)
+          replay_paths_log<DL, LOG_GEOPUT_IZ>(M, s_start, log_strike, P.m, P.n_steps, rec, P.n_inner, p0, p1, vals,
+                                              P.steps);
+        else
+          walk_paths_log<DL, LOG_GEOPUT_IZ, true>(M, s_start, log_strike, P.m, P.n_steps, key, stream, base0, p0, p1,
+                                                  vals, nullptr, &s_next, P.steps, tq, rec, P.n_inner);
+      } else if constexpr (GEOK == 2) {
         walk_paths_log<(D > 1 ? D : 2), LOG_GEOPUT_IZ>(M, s_start, log_strike, P.m, P.n_steps, key, stream, base0, p0,
                                                        p1, vals, nullptr, &s_next, P.steps, tq);
-      else
+      } else {
         walk_paths<D, FAST, GEOK ? WALK_GEO : WALK_GENERIC>(M, s_start, P.m, P.n_steps, key, stream, base0, p0, p1,
                                                             ns, vals, &s_next, nullptr, nullptr, P.steps, tq);
+      }
     }
     __syncthreads();
     // fixed-order fold in 256-path chunks: the chunk sums are added in path
@@ -332,13 +364,11 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
     // cluster size (i.e. on how many probes share the GPU)
     fold_chunks(vals, p1 > p0 ? p1 - p0 : 0, s_chunk);
     cluster.sync();
+    int n_chunks = 0;
+    if (rank == 0 && threadIdx.x < 32) n_chunks = gather_chunk_sums(cluster, s_chunk, csize, per_cta, P.n_inner, s_all);
     if (rank == 0 && threadIdx.x == 0) {
       double total = 0.0;
-      for (int r = 0; r < csize; ++r) {
-        const double *rc = cluster.map_shared_rank(s_chunk, r);
-        for (int c = 0; r * per_cta + c * kIzFoldChunk < min((r + 1) * per_cta, P.n_inner); ++c)
-          total = __dadd_rn(total, rc[c]);
-      }
+      for (int g = 0; g < n_chunks; ++g) total = __dadd_rn(total, s_all[g]);
       const double cont = __ddiv_rn(total, (double)P.n_inner);
       const int n_it = it + 1;
       s_it = n_it;

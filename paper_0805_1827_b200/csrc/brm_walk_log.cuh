@@ -129,9 +129,12 @@ __device__ __forceinline__ bool cmc_stop_log(const Model<double> &M, int m, cons
 // step_draws_compact) the log-prices of the group's assets step at once, so
 // only one group of normals is live.  Queue slots come from one ballot per
 // draw (the rank of the lane among the lanes whose draw is a tail draw).
+// inc (optional): the step's increments mu_i + vol_i z_i, for the draw cache
+// of the bisection probes (iz_probes, brm_kernels.cuh).
 template <int D, bool EVEN>
 __device__ __forceinline__ void step_log_prices(const Model<double> &M, const PhiloxKey &K, uint64_t idx0, double *x,
-                                                bool active, double *wbuf, unsigned short *widx, unsigned lt_mask) {
+                                                bool active, double *wbuf, unsigned short *widx, unsigned lt_mask,
+                                                double *inc = nullptr) {
   constexpr int NC = EVEN ? D / 2 : D / 2 + 1;
   constexpr int G = TailGroup<D>::G;
   static_assert(D % G == 0, "the log-price walker steps whole draw groups");
@@ -186,7 +189,11 @@ __device__ __forceinline__ void step_log_prices(const Model<double> &M, const Ph
       __syncwarp();
     }
 #pragma unroll
-    for (int a = g0; a < g0 + G; ++a) x[a] = r_add(x[a], fma(M.vol[a], z[a], M.mu[a]));
+    for (int a = g0; a < g0 + G; ++a) {
+      const double dx = fma(M.vol[a], z[a], M.mu[a]);
+      if (inc) inc[a] = dx;
+      x[a] = r_add(x[a], dx);
+    }
   }
 }
 
@@ -204,17 +211,54 @@ __device__ __forceinline__ bool iz_stop_log(const Model<double> &M, int m, const
   return x[D - 1] <= quad_surface<D>(row, w, k);
 }
 
+// Decision of a path at date m in state x: true when it stops; xstop is then
+// x_max (LOG_MAXCALL_CMC; the payoff is formed by finish_log_values) or the
+// discounted payoff itself (LOG_GEOPUT_IZ).
+template <int D, int KIND>
+__device__ __forceinline__ bool log_state_stops(const Model<double> &M, double log_strike, int m, int m_start,
+                                                const double *x, double &xstop) {
+  if constexpr (KIND == LOG_GEOPUT_IZ) {
+    // geometric mean in log space: the same sequential sum and divide as geo_payoff (brm_walk.cuh)
+    double sx = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) sx = r_add(sx, x[i]);
+    const double g = __ddiv_rn(sx, (double)D);
+    const double dk = r_sub(log_strike, g);
+    bool itm = dk > 0.0;
+    if (fabs(dk) <= 1e-13) itm = r_sub(M.strike, exp_nb(g)) > 0.0;  // decide at the money in price space
+    const bool stop = itm && (m == M.n_dates || iz_stop_log<D>(M, m, x));
+    if (stop) xstop = r_mul(r_sub(M.strike, exp_nb(g)), M.disc[m - m_start]);
+    return stop;
+  } else {
+    double xmax = x[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i)
+      if (x[i] > xmax) xmax = x[i];
+    const double dk = r_sub(xmax, log_strike);
+    bool itm = dk > 0.0;
+    if (fabs(dk) <= 1e-13) itm = r_sub(exp_nb(xmax), M.strike) > 0.0;  // decide at the money in price space
+    const bool stop = itm && (m == M.n_dates || cmc_stop_log<D>(M, m, x, xmax));
+    if (stop) xstop = xmax;
+    return stop;
+  }
+}
+
 // Walk paths [p0, p1) of one unit from the shared start log-prices x_start
 // (lane refill as walk_paths, brm_walk.cuh).
+// RECORD (bisection probes, first pass): every path is stepped to expiry and
+// its increments go to rec[(k * rec_paths + p) * D + i] (a plane per step,
+// paths contiguous: a warp's replay loads cover a contiguous 32 D doubles);
+// the value is that of the path's first stop.  The later passes replay them
+// (replay_paths_log).
 // LOG_MAXCALL_CMC: slot p - p0 of vals receives the stopped path's x_max and
 // stopm its stop date (0: expired worthless); finish_log_values turns them
 // into discounted payoffs.  LOG_GEOPUT_IZ: vals receives the discounted payoff
 // itself (stopm unused; the probe clusters fold vals as they are).
-template <int D, int KIND = LOG_MAXCALL_CMC>
+template <int D, int KIND = LOG_MAXCALL_CMC, bool RECORD = false>
 __device__ void walk_paths_log(const Model<double> &M, const double *x_start, double log_strike, int m_start,
                                int n_steps, uint64_t key, uint64_t stream, uint64_t base0, int p0, int p1,
                                double *vals, unsigned char *stopm, int *s_next, unsigned long long *step_count,
-                               const TailQueue &tq) {
+                               const TailQueue &tq, double *rec = nullptr, int rec_paths = 0) {
   static_assert(D > 1, "the log-price walkers are d > 1 instances");
   const uint64_t stride = (uint64_t)n_steps * (uint64_t)D;
   const unsigned lane = threadIdx.x & 31;
@@ -229,6 +273,9 @@ __device__ void walk_paths_log(const Model<double> &M, const double *x_start, do
   uint64_t base = base0 + (uint64_t)(have ? p : 0) * stride;
 #pragma unroll
   for (int i = 0; i < D; ++i) x[i] = x_start[i];
+  [[maybe_unused]] bool stopped = false;  // RECORD: the path's first stop is kept while it steps on
+  [[maybe_unused]] double xkeep = 0.0;
+  [[maybe_unused]] int mkeep = 0;
 
   while (__any_sync(0xffffffffu, have)) {
     bool done = false;
@@ -236,34 +283,28 @@ __device__ void walk_paths_log(const Model<double> &M, const double *x_start, do
     int stop_m = 0;
     // the whole warp draws (the tail pass is warp-cooperative); lanes without
     // a path step a dummy state at a valid index and discard it
-    step_log_prices<D, D % 2 == 0>(M, K, base + (uint64_t)k * (uint64_t)D, x, have, tq.buf, tq.idx, lt_mask);
+    [[maybe_unused]] double inc[D];
+    step_log_prices<D, D % 2 == 0>(M, K, base + (uint64_t)k * (uint64_t)D, x, have, tq.buf, tq.idx, lt_mask,
+                                   RECORD ? inc : nullptr);
     if (have) {
       ++nsteps;
       const int m = m_start + k + 1;
-      bool stop;
-      if constexpr (KIND == LOG_GEOPUT_IZ) {
-        // geometric mean in log space: the same sequential sum and divide as geo_payoff (brm_walk.cuh)
-        double sx = 0.0;
+      if constexpr (RECORD) {
+        double *dst = rec + ((size_t)k * rec_paths + p) * D;
 #pragma unroll
-        for (int i = 0; i < D; ++i) sx = r_add(sx, x[i]);
-        const double g = __ddiv_rn(sx, (double)D);
-        const double dk = r_sub(log_strike, g);
-        bool itm = dk > 0.0;
-        if (fabs(dk) <= 1e-13) itm = r_sub(M.strike, exp_nb(g)) > 0.0;  // decide at the money in price space
-        stop = itm && (m == M.n_dates || iz_stop_log<D>(M, m, x));
-        if (stop) xstop = r_mul(r_sub(M.strike, exp_nb(g)), M.disc[m - m_start]);
-      } else {
-        double xmax = x[0];
-#pragma unroll
-        for (int i = 1; i < D; ++i)
-          if (x[i] > xmax) xmax = x[i];
-        const double dk = r_sub(xmax, log_strike);
-        bool itm = dk > 0.0;
-        if (fabs(dk) <= 1e-13) itm = r_sub(exp_nb(xmax), M.strike) > 0.0;  // decide at the money in price space
-        stop = itm && (m == M.n_dates || cmc_stop_log<D>(M, m, x, xmax));
-        if (stop) xstop = xmax;
-      }
-      if (stop) {
+        for (int i = 0; i < D; ++i) dst[i] = inc[i];
+        if (!stopped && log_state_stops<D, KIND>(M, log_strike, m, m_start, x, xkeep)) {
+          stopped = true;
+          mkeep = m;
+        }
+        if (k + 1 == n_steps) {
+          done = true;
+          xstop = xkeep;
+          stop_m = mkeep;
+        } else {
+          ++k;
+        }
+      } else if (log_state_stops<D, KIND>(M, log_strike, m, m_start, x, xstop)) {
         stop_m = m;
         done = true;
       } else if (k + 1 == n_steps) {
@@ -289,6 +330,11 @@ __device__ void walk_paths_log(const Model<double> &M, const double *x_start, do
         base = base0 + (uint64_t)(have ? p : 0) * stride;
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = x_start[i];
+        if constexpr (RECORD) {
+          stopped = false;
+          xkeep = 0.0;
+          mkeep = 0;
+        }
       }
     }
   }
@@ -297,6 +343,67 @@ __device__ void walk_paths_log(const Model<double> &M, const double *x_start, do
     for (int off = 16; off > 0; off >>= 1) nsteps += __shfl_down_sync(0xffffffffu, nsteps, off);
     if (lane == 0 && nsteps) atomicAdd(step_count, (unsigned long long)nsteps);
   }
+}
+
+// Bisection probes, passes after the first (common random numbers: every pass
+// walks the same paths from another start state): path p's log-prices are
+// x_start + the recorded increments, added in step order exactly as
+// walk_paths_log adds them, so a replayed pass returns the bits a re-simulated
+// pass would -- without drawing a single normal.  Paths are assigned to
+// threads statically (a replayed path-step is ~80 instructions and a
+// coalesced read of D doubles); vals as walk_paths_log.
+#ifndef BRM_REPLAY_B
+#define BRM_REPLAY_B 1
+#endif
+template <int D, int KIND>
+__device__ __forceinline__ void replay_paths_log(const Model<double> &M, const double *x_start, double log_strike,
+                                                 int m_start, int n_steps, const double *rec, int rec_paths, int p0,
+                                                 int p1, double *vals, unsigned long long *step_count) {
+  // a thread replays B of its paths together, step by step, with the next
+  // step's increments in flight while this step is decided.  Measured on C2
+  // (64 probes x 5000 paths): B = 1 5.4 ms of probe kernels per price, B = 2
+  // 5.9 ms, B = 4 6.5 ms (spills) -- the replays stream the cache at ~4 TB/s,
+  // they are not bound by the per-thread chain.
+  constexpr int B = BRM_REPLAY_B;
+  const size_t plane = (size_t)rec_paths * D;
+  for (int q0 = p0 + threadIdx.x; q0 < p1; q0 += B * blockDim.x) {
+    double x[B][D], nxt[B][D], val[B];
+    bool live[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      live[b] = q0 + b * (int)blockDim.x < p1;
+      val[b] = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        x[b][i] = x_start[i];
+        nxt[b][i] = live[b] ? __ldcg(rec + (size_t)(q0 + b * (int)blockDim.x) * D + i) : 0.0;
+      }
+    }
+    for (int k = 0; k < n_steps; ++k) {
+      bool any = false;
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        any |= live[b];
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[b][i] = r_add(x[b][i], nxt[b][i]);
+      }
+      if (!any) break;
+      if (k + 1 < n_steps) {
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+            if (live[b]) nxt[b][i] = __ldcg(rec + (size_t)(k + 1) * plane + (size_t)(q0 + b * (int)blockDim.x) * D + i);
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (live[b] && log_state_stops<D, KIND>(M, log_strike, m_start + k + 1, m_start, x[b], val[b])) live[b] = false;
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (q0 + b * (int)blockDim.x < p1) vals[q0 + b * (int)blockDim.x - p0] = val[b];
+  }
+  (void)step_count;  // replayed steps draw nothing: they are not counted as simulated path-steps
 }
 
 // (x_max, stop date) of every path of the chunk -> discounted payoff

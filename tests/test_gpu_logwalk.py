@@ -130,3 +130,30 @@ def test_log_walker_equals_price_stepper(tmp_path):
         outs.append(np.load(out))
     assert np.array_equal(outs[0]["m"], outs[1]["m"])
     assert np.all(np.abs(outs[0]["v"] - outs[1]["v"]) <= 1e-13 * 100.0)
+
+
+@pytest.mark.parametrize("d", [2, 5])
+def test_geoput_probe_bisection_log_walker_and_draw_cache(d, monkeypatch):
+    """The geometric put's probe clusters on log-prices (iz_probes<.., 2 / 3>): sequential bisection
+    (tree off) with the draw cache -- first pass records the increments, the others replay them --
+    returns the bits of the re-simulating kernel, and both agree with the oracle's price-space
+    bisection (iteration counts and flags equal, levels to 1e-9 K)."""
+    p, s = CS.geoput(d)
+    mp = CS.packs(p, s)
+    rp = CS.random_surfaces(d, s.n_dates, 100.0, seed=6, iz_space=1, call_like=False)
+    n = 6
+    seeds = np.random.default_rng(4).uniform(60, 140, size=(n, d - 1))
+    keys, strs = zip(*[O.derive_words(5, 1, i, 3) for i in range(n)])
+    monkeypatch.setenv("BRM_IZ_NO_TREE", "1")
+    args = dict(solver="bisection", lo=50.0, hi=100.0, tol=1e-4, max_iter=100, keys=keys, streams=strs,
+                mode="parity")
+    cached = G.iz_solve_batch(mp, rp, seeds, [d - 1] * n, 3, 1500, **args)
+    monkeypatch.setenv("BRM_IZ_NO_CACHE", "1")
+    plain = G.iz_solve_batch(mp, rp, seeds, [d - 1] * n, 3, 1500, **args)
+    for a, b in zip(cached, plain):
+        assert np.array_equal(a, b)
+    octx = O.Ctx(mp, rp)
+    for i in range(n):
+        ol, oi, oc = O.iz_bisect(octx, seeds[i], d - 1, 3, 1500, 50.0, 100.0, 1e-4, 100, keys[i], strs[i])
+        assert cached[1][i] == oi and cached[2][i] == oc
+        assert abs(cached[0][i] - ol) <= 1e-9 * max(abs(ol), mp.strike)
