@@ -698,6 +698,8 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       // Compute cannot replay cooperative cluster launches); same results
       const bool ncu_safe = getenv("BRM_NCU_SAFE") != nullptr;
       if (ncu_safe) cl = 1;
+      // BRM_BOOST_CL: cap the cluster size (A/B runs of the sync / work-per-thread trade)
+      if (const char *e = getenv("BRM_BOOST_CL")) cl = std::max(1, std::min(cl, atoi(e)));
       const int L = (int)tree.leaves.size();
       // (slice_cap, pos_cap, dynamic shared memory) for cluster size c
       auto layout = [&](int c, int &slice_cap, int &pos_cap) {

@@ -1301,11 +1301,20 @@ int brm_iz_solve(brm_ctx *c, int32_t solver, const double *seeds, const int32_t 
   P.rec = nullptr;
   if (solver == 1 && P.tree_levels == 1 && kiz == c->kern.iz_geo_log && c->kern.iz_geo_log_rec && P.max_iter > 1 &&
       getenv("BRM_IZ_NO_CACHE") == nullptr) {
-    const size_t cells = (size_t)n * P.n_steps * n_inner * c->hdr.d;
-    if (cells <= ((size_t)1 << 28)) {  // <= 2 GB
-      BRM_TRY(call.scratch<double>(cells, &P.rec));
-      kiz = c->kern.iz_geo_log_rec;  // same launch shape and shared memory
-      BRM_TRY(allow_smem(kiz, smem));
+    const size_t cells = (size_t)n * P.n_steps * n_inner * 3;
+    // a replay pass keeps the values of kIzReplayCand candidate levels per path in shared memory
+    const int hist_rec = P.vals_offset + ((8 * kIzReplayCand * per_cta + 15) & ~15);
+    const int smem_rec = hist_rec + 8 * (P.max_iter + 1);
+    if (cells <= ((size_t)1 << 28) && smem_rec <= 88 * 1024) {  // <= 2 GB; two CTAs per SM with the static arrays
+      if (call.scratch<double>(cells, &P.rec) == BRM_OK && P.rec) {
+        kiz = c->kern.iz_geo_log_rec;  // same launch shape
+        P.hist_offset = hist_rec;
+        cfg.dynamicSmemBytes = smem_rec;
+        BRM_TRY(allow_smem(kiz, smem_rec));
+      } else {  // no room for the cache: every pass re-simulates
+        P.rec = nullptr;
+        cudaGetLastError();
+      }
     }
   }
   void *args[] = {&P};

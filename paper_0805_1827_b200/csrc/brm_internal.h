@@ -15,6 +15,8 @@ constexpr int kPriceChunk = 2048;   // paths per pricing work item (2 per block:
 constexpr int kMaxChunk = 2048;     // largest chunk a walker CTA folds in smem
 constexpr int kIzFoldChunk = 256;   // I&Z probes: paths per fixed-order fold chunk
 constexpr int kIzMaxChunks = 64;    // fold chunks per probe CTA (16384 inner paths)
+constexpr int kIzReplayLevels = 3;  // bisection levels a replay pass of the draw cache decides ...
+constexpr int kIzReplayCand = (1 << kIzReplayLevels) - 1;  // ... from that many candidate levels
 
 // Inner paths per CTA of an I&Z probe cluster: whole fold chunks, so the
 // chunk boundaries (and the summation order) do not depend on the cluster size.
@@ -81,9 +83,9 @@ struct IzParams {
   // per pass on as many clusters (cooperative launch), tree_passes passes
   int tree_levels, tree_passes;
   double *tree_cont;  // [2][n_probes][2^L - 1] node continuation values
-  // bisection draw cache (log-price probe walker, sequential bisection): the
-  // first pass records every path's increments, [n_probes][n_steps][n_inner][d];
-  // the later passes replay them (null: every pass re-simulates)
+  // bisection draw cache (log-price probe walker of the geometric put,
+  // sequential bisection): the first pass records every path,
+  // [n_probes][n_steps][n_inner][3] (brm_walk_log.cuh); the later passes replay
   double *rec;
 };
 

@@ -161,6 +161,24 @@ __device__ __forceinline__ int gather_chunk_sums(cg::cluster_group &cluster, dou
   return n_chunks;
 }
 
+// fold_chunks for n_cand value arrays (vals + t * stride -> s_chunk + t * kIzMaxChunks): the
+// (candidate, chunk) pairs go round the warps, one barrier for all of them.
+__device__ __forceinline__ void fold_chunks_multi(const double *vals, int stride, int n_cand, int n, double *s_chunk) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nck = (n + kIzFoldChunk - 1) / kIzFoldChunk;
+  for (int q = warp; q < n_cand * nck; q += blockDim.x >> 5) {
+    const int t = q / nck, c = q - t * nck;
+    const double *v = vals + (size_t)t * stride + c * kIzFoldChunk;
+    const int len = min(kIzFoldChunk, n - c * kIzFoldChunk);
+    double s = 0.0;
+    for (int j = lane; j < len; j += 32) s = __dadd_rn(s, v[j]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
+    if (lane == 0) s_chunk[t * kIzMaxChunks + c] = s;
+  }
+  __syncthreads();
+}
+
 // GMODE 1: the geometric-put instance (walk_paths' GEO step; launched only for
 // that payoff).  GMODE 2: the geometric put on log-prices (walk_paths_log's
 // LOG_GEOPUT_IZ; parity mode, log-space I&Z surface, independent assets).
@@ -188,7 +206,8 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
   __shared__ int s_next;
   __shared__ R s_start[kMaxD];
   __shared__ double s_state[kMaxD];
-  __shared__ double s_chunk[kIzMaxChunks];  // this CTA's 256-path chunk sums
+  constexpr int kCand = GMODE == 3 ? kIzReplayCand : 1;  // candidate levels a pass evaluates
+  __shared__ double s_chunk[kCand * kIzMaxChunks];  // this CTA's 256-path chunk sums (per candidate)
   __shared__ double s_all[kIzMaxChunks * 8];  // rank 0: every CTA's chunk sums in path order
   __shared__ double s_x, s_lo, s_hi;        // rank 0: solver state
   __shared__ int s_done, s_it, s_armed, s_conv;
@@ -327,6 +346,112 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
     return;
   }
 
+  if constexpr (GMODE == 3) {
+    // ---- sequential bisection over a draw cache (solver 1, geometric put) ----
+    // Bisection evaluates every candidate level with the same draws, so pass 0
+    // walks the paths once from the first midpoint and records them
+    // (walk_paths_log's RECORD), and every later pass replays the record for
+    // the 2^L - 1 midpoints of the next L bisection levels at once
+    // (replay_geoput_log) and then takes those L decisions: the same
+    // midpoints (the same fp64 operations), continuation values, decisions
+    // and iteration count as one level per pass, in 1 + (levels - 1) / L passes.
+    constexpr int DL = D > 1 ? D : 2;
+    constexpr int TL = kIzReplayLevels, T = kIzReplayCand;
+    __shared__ double s_xl0[T], s_xm[T], s_pay[T], s_cont[T];
+    double *rec = P.rec + (size_t)probe * P.n_steps * P.n_inner * 3;
+    double *lo_remote = cluster.map_shared_rank(&s_lo, 0), *hi_remote = cluster.map_shared_rank(&s_hi, 0);
+    for (int pass = 0;; ++pass) {
+      if (*done_remote) break;
+      const double lo = *lo_remote, hi = *hi_remote;  // rank 0 moves the bracket between the two barriers below only
+      const int n_cand = pass == 0 ? 1 : T;
+      if ((int)threadIdx.x < n_cand) {
+        // node t of the complete tree of midpoints below (lo, hi), by the heap path
+        double l = lo, h = hi;
+        const int path = (int)threadIdx.x + 1;
+        for (int tt = 31 - __clz(path) - 1; tt >= 0; --tt) {
+          const double xm = __dmul_rn(0.5, __dadd_rn(l, h));
+          if ((path >> tt) & 1) l = xm;
+          else h = xm;
+        }
+        const double xm = __dmul_rn(0.5, __dadd_rn(l, h));
+        double st[kMaxD];
+        probe_state(P.hdr, seedp, asset, xm, st);
+        s_xm[threadIdx.x] = xm;
+        s_xl0[threadIdx.x] = log(st[d - 1]);
+        {
+          Model<double> Md{};
+          Md.d = d;
+          Md.payoff = P.hdr.payoff;
+          Md.strike = K;
+          s_pay[threadIdx.x] = payoff<0>(Md, st);  // the level's exercise value (the bisection's other side)
+        }
+        if (pass == 0)
+          for (int i = 0; i < d; ++i) s_state[i] = st[i];
+      }
+      __syncthreads();
+      if (pass == 0) {
+        if (threadIdx.x < d) s_start[threadIdx.x] = log(s_state[threadIdx.x]);
+        if (threadIdx.x == 0) s_next = p0 + blockDim.x;
+        __syncthreads();
+        if (p0 < p1)
+          walk_paths_log<DL, LOG_GEOPUT_IZ, true>(M, s_start, log_strike, P.m, P.n_steps, key, stream,
+                                                  unit_base<FAST>(0, false), p0, p1, vals, nullptr, &s_next, P.steps,
+                                                  tq, rec, P.n_inner);
+      } else if (p0 < p1) {
+        replay_geoput_log<DL, T>(M, log_strike, P.m, P.n_steps, rec, P.n_inner, p0, p1, s_xl0, n_cand, vals, per_cta);
+      }
+      __syncthreads();
+      fold_chunks_multi(vals, per_cta, n_cand, p1 > p0 ? p1 - p0 : 0, s_chunk);
+      cluster.sync();
+      if (rank == 0 && threadIdx.x < 32) {
+        // every candidate's chunk sums over DSMEM, all remote loads in flight together when they
+        // fit s_all (candidate-major), else candidate by candidate
+        const int n_chunks = (P.n_inner + kIzFoldChunk - 1) / kIzFoldChunk;
+        const int per_cta_chunks = per_cta / kIzFoldChunk;
+        const bool together = n_cand * n_chunks <= kIzMaxChunks * 8;
+        if (together) {
+          for (int q = threadIdx.x; q < n_cand * n_chunks; q += 32) {
+            const int t = q / n_chunks, g = q - t * n_chunks, r = g / per_cta_chunks;
+            s_all[q] = cluster.map_shared_rank(s_chunk, r)[t * kIzMaxChunks + g - r * per_cta_chunks];
+          }
+          __syncwarp();
+        }
+        for (int t = 0; t < n_cand; ++t) {
+          if (!together) gather_chunk_sums(cluster, s_chunk + t * kIzMaxChunks, csize, per_cta, P.n_inner, s_all);
+          if (threadIdx.x == 0) {
+            const double *cs = together ? s_all + t * n_chunks : s_all;
+            double total = 0.0;
+            for (int g = 0; g < n_chunks; ++g) total = __dadd_rn(total, cs[g]);
+            s_cont[t] = __ddiv_rn(total, (double)P.n_inner);
+          }
+          __syncwarp();
+        }
+        if (threadIdx.x == 0) {
+          double l = s_lo, h = s_hi;
+          int j = 0, n_it = s_it;
+          bool fin = false;
+          for (int lev = 0; lev < (pass == 0 ? 1 : TL) && !fin; ++lev) {
+            const double xm = s_xm[j];  // == 0.5 (l + h): the node's midpoint
+            const bool exercise = __dsub_rn(s_pay[j], s_cont[j]) > 0.0;
+            if (call_like == exercise) {
+              h = xm;
+              j = 2 * j + 1;
+            } else {
+              l = xm;
+              j = 2 * j + 2;
+            }
+            ++n_it;
+            fin = !(__dsub_rn(h, l) > P.tol) || n_it >= P.max_iter;
+          }
+          s_lo = l;
+          s_hi = h;
+          s_it = n_it;
+          if (fin) s_done = 1;
+        }
+      }
+      cluster.sync();
+    }
+  } else
   for (int it = 0;; ++it) {
     if (*done_remote) break;
     const double x = *x_remote;
@@ -340,16 +465,7 @@ __global__ void __launch_bounds__(kWalkThreads, 2) iz_probes(IzParams P) {
     const uint64_t base0 = unit_base<FAST>(draw_base, P.normals != nullptr);
     if (p0 < p1) {
       if constexpr (GMODE == 3) {
-        // bisection walks the same paths every pass (common random numbers): the first pass
-        // records their increments and the others replay them
-        constexpr int DL = D > 1 ? D : 2;
-        double *rec = P.rec + (size_t)probe * P.n_steps * P.n_inner * d;
-        if (it > 0)
-          replay_paths_log<DL, LOG_GEOPUT_IZ>(M, s_start, log_strike, P.m, P.n_steps, rec, P.n_inner, p0, p1, vals,
-                                              P.steps);
-        else
-          walk_paths_log<DL, LOG_GEOPUT_IZ, true>(M, s_start, log_strike, P.m, P.n_steps, key, stream, base0, p0, p1,
-                                                  vals, nullptr, &s_next, P.steps, tq, rec, P.n_inner);
+        // (handled by the draw-cache solver above)
       } else if constexpr (GEOK == 2) {
         walk_paths_log<(D > 1 ? D : 2), LOG_GEOPUT_IZ>(M, s_start, log_strike, P.m, P.n_steps, key, stream, base0, p0,
                                                        p1, vals, nullptr, &s_next, P.steps, tq);

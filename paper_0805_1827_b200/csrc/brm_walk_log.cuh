@@ -202,13 +202,18 @@ enum { LOG_MAXCALL_CMC = 0, LOG_GEOPUT_IZ = 1 };
 // Log-space boundary decision of the geometric put (iz_stop's iz_space == 1
 // branch, brm_model.cuh, on the state's own log-prices).
 template <int D>
-__device__ __forceinline__ bool iz_stop_log(const Model<double> &M, int m, const double *x) {
+__device__ __forceinline__ double iz_surface_log(const Model<double> &M, int m, const double *x) {
   constexpr int k = D - 1;
   double w[k];
 #pragma unroll
   for (int j = 0; j < k; ++j) w[j] = x[j] < M.izlo[j] ? M.izlo[j] : (x[j] > M.izhi[j] ? M.izhi[j] : x[j]);
   const double *row = M.izc + ((size_t)m * D + (D - 1)) * M.nbasis;
-  return x[D - 1] <= quad_surface<D>(row, w, k);
+  return quad_surface<D>(row, w, k);
+}
+
+template <int D>
+__device__ __forceinline__ bool iz_stop_log(const Model<double> &M, int m, const double *x) {
+  return x[D - 1] <= iz_surface_log<D>(M, m, x);
 }
 
 // Decision of a path at date m in state x: true when it stops; xstop is then
@@ -245,11 +250,16 @@ __device__ __forceinline__ bool log_state_stops(const Model<double> &M, double l
 
 // Walk paths [p0, p1) of one unit from the shared start log-prices x_start
 // (lane refill as walk_paths, brm_walk.cuh).
-// RECORD (bisection probes, first pass): every path is stepped to expiry and
-// its increments go to rec[(k * rec_paths + p) * D + i] (a plane per step,
-// paths contiguous: a warp's replay loads cover a contiguous 32 D doubles);
-// the value is that of the path's first stop.  The later passes replay them
-// (replay_paths_log).
+// RECORD (bisection probes of the geometric put, first pass): every path is
+// stepped to expiry and leaves, per step, what the later passes need -- they
+// differ from this one only in the start of the probed (last) asset:
+//   rec[(k * rec_paths + p) * 3 + 0]  the last asset's increment mu + vol z
+//   rec[... + 1]  the other assets' log-price sum, ((0 + x_0) + x_1) + ...
+//                 (the leading part of geo_payoff's sequential sum)
+//   rec[... + 2]  the boundary surface over the other assets' log-prices
+//                 (+inf at expiry: any in-the-money path stops)
+// (a plane per step, paths contiguous: a warp's replay loads are coalesced).
+// The value is that of the path's first stop.  replay_geoput_log replays.
 // LOG_MAXCALL_CMC: slot p - p0 of vals receives the stopped path's x_max and
 // stopm its stop date (0: expired worthless); finish_log_values turns them
 // into discounted payoffs.  LOG_GEOPUT_IZ: vals receives the discounted payoff
@@ -290,9 +300,14 @@ __device__ void walk_paths_log(const Model<double> &M, const double *x_start, do
       ++nsteps;
       const int m = m_start + k + 1;
       if constexpr (RECORD) {
-        double *dst = rec + ((size_t)k * rec_paths + p) * D;
+        static_assert(!RECORD || KIND == LOG_GEOPUT_IZ, "the draw cache is the geometric put's");
+        double *dst = rec + ((size_t)k * rec_paths + p) * 3;
+        double sa = 0.0;
 #pragma unroll
-        for (int i = 0; i < D; ++i) dst[i] = inc[i];
+        for (int i = 0; i < D - 1; ++i) sa = r_add(sa, x[i]);
+        dst[0] = inc[D - 1];
+        dst[1] = sa;
+        dst[2] = m == M.n_dates ? __longlong_as_double(0x7ff0000000000000LL) : iz_surface_log<D>(M, m, x);
         if (!stopped && log_state_stops<D, KIND>(M, log_strike, m, m_start, x, xkeep)) {
           stopped = true;
           mkeep = m;
@@ -352,58 +367,79 @@ __device__ void walk_paths_log(const Model<double> &M, const double *x_start, do
 // pass would -- without drawing a single normal.  Paths are assigned to
 // threads statically (a replayed path-step is ~80 instructions and a
 // coalesced read of D doubles); vals as walk_paths_log.
-#ifndef BRM_REPLAY_B
-#define BRM_REPLAY_B 1
-#endif
-template <int D, int KIND>
-__device__ __forceinline__ void replay_paths_log(const Model<double> &M, const double *x_start, double log_strike,
-                                                 int m_start, int n_steps, const double *rec, int rec_paths, int p0,
-                                                 int p1, double *vals, unsigned long long *step_count) {
-  // a thread replays B of its paths together, step by step, with the next
-  // step's increments in flight while this step is decided.  Measured on C2
-  // (64 probes x 5000 paths): B = 1 5.4 ms of probe kernels per price, B = 2
-  // 5.9 ms, B = 4 6.5 ms (spills) -- the replays stream the cache at ~4 TB/s,
-  // they are not bound by the per-thread chain.
-  constexpr int B = BRM_REPLAY_B;
-  const size_t plane = (size_t)rec_paths * D;
-  for (int q0 = p0 + threadIdx.x; q0 < p1; q0 += B * blockDim.x) {
-    double x[B][D], nxt[B][D], val[B];
-    bool live[B];
+// Bisection probes of the geometric put, passes after the first (common random
+// numbers: every pass walks the same paths, from start states that differ in
+// the probed asset only).  A thread replays its paths (static assignment) for
+// n_cand candidate levels at once -- the midpoints of the next bisection
+// levels -- from one read of the record: per step and candidate
+//   xl += inc;  s = sa + xl;  g = s / D;  stop iff g < log K and xl <= b,
+// the operations, in the order, of walk_paths_log's LOG_GEOPUT_IZ step, so a
+// candidate's values are the bits a re-simulated pass would produce, without
+// drawing a normal or evaluating a surface.  xl0[t]: the probed asset's start
+// log-price of candidate t; vals[t * stride + (p - p0)] receives the values.
+template <int D, int T>
+__device__ __forceinline__ void replay_geoput_log(const Model<double> &M, double log_strike, int m_start, int n_steps,
+                                                  const double *rec, int rec_paths, int p0, int p1, const double *xl0,
+                                                  int n_cand, double *vals, int stride) {
+  const size_t plane = (size_t)rec_paths * 3;
+  for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+    double xl[T], val[T];
+    unsigned live = n_cand >= 32 ? 0xffffffffu : (1u << n_cand) - 1u;
 #pragma unroll
-    for (int b = 0; b < B; ++b) {
-      live[b] = q0 + b * (int)blockDim.x < p1;
-      val[b] = 0.0;
+    for (int t = 0; t < T; ++t) {
+      xl[t] = xl0[t < n_cand ? t : 0];
+      val[t] = 0.0;
+    }
+    const double *src = rec + (size_t)p * 3;
+    double inc = __ldcg(src), sa = __ldcg(src + 1), b = __ldcg(src + 2);
+    for (int k = 0; k < n_steps && live; ++k) {
+      const double cinc = inc, csa = sa, cb = b;
+      if (k + 1 < n_steps) {  // the next step's record is in flight while this one is decided
+        inc = __ldcg(src + (size_t)(k + 1) * plane);
+        sa = __ldcg(src + (size_t)(k + 1) * plane + 1);
+        b = __ldcg(src + (size_t)(k + 1) * plane + 2);
+      }
+      // the T candidates are independent chains: straight-line code for the decisions (their
+      // divides interleave), one branch for the rare at-the-money guard, one for the stops
+      double g[T];
+      unsigned stops = 0, near = 0;
 #pragma unroll
-      for (int i = 0; i < D; ++i) {
-        x[b][i] = x_start[i];
-        nxt[b][i] = live[b] ? __ldcg(rec + (size_t)(q0 + b * (int)blockDim.x) * D + i) : 0.0;
+      for (int t = 0; t < T; ++t) {
+        xl[t] = r_add(xl[t], cinc);
+        // (div_nb: __ddiv_rn's bits for normal operands -- a sum of log-prices over D; a sum
+        // next to zero takes the guard's library path)
+        const double sx = r_add(csa, xl[t]);
+        g[t] = div_nb(sx, (double)D);
+        const double dk = r_sub(log_strike, g[t]);
+        near |= ((fabs(dk) <= 1e-13 || !(fabs(sx) >= 0x1p-1000)) ? 1u : 0u) << t;
+        stops |= ((dk > 0.0 && xl[t] <= cb) ? 1u : 0u) << t;
+      }
+      near &= live;
+      if (near) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          if ((near >> t) & 1u) {
+            g[t] = __ddiv_rn(r_add(csa, xl[t]), (double)D);
+            const double dk = r_sub(log_strike, g[t]);
+            bool itm = dk > 0.0;
+            if (fabs(dk) <= 1e-13) itm = r_sub(M.strike, exp_nb(g[t])) > 0.0;  // decide at the money in price space
+            stops = (stops & ~(1u << t)) | ((itm && xl[t] <= cb) ? 1u << t : 0u);
+          }
+        }
+      }
+      stops &= live;
+      if (stops) {
+        const double disc = M.disc[k + 1];
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+          if ((stops >> t) & 1u) val[t] = r_mul(r_sub(M.strike, exp_nb(g[t])), disc);
+        live &= ~stops;
       }
     }
-    for (int k = 0; k < n_steps; ++k) {
-      bool any = false;
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        any |= live[b];
-#pragma unroll
-        for (int i = 0; i < D; ++i) x[b][i] = r_add(x[b][i], nxt[b][i]);
-      }
-      if (!any) break;
-      if (k + 1 < n_steps) {
-#pragma unroll
-        for (int b = 0; b < B; ++b)
-#pragma unroll
-          for (int i = 0; i < D; ++i)
-            if (live[b]) nxt[b][i] = __ldcg(rec + (size_t)(k + 1) * plane + (size_t)(q0 + b * (int)blockDim.x) * D + i);
-      }
-#pragma unroll
-      for (int b = 0; b < B; ++b)
-        if (live[b] && log_state_stops<D, KIND>(M, log_strike, m_start + k + 1, m_start, x[b], val[b])) live[b] = false;
-    }
-#pragma unroll
-    for (int b = 0; b < B; ++b)
-      if (q0 + b * (int)blockDim.x < p1) vals[q0 + b * (int)blockDim.x - p0] = val[b];
+    for (int t = 0; t < T; ++t)
+      if (t < n_cand) vals[(size_t)t * stride + (p - p0)] = val[t];
   }
-  (void)step_count;  // replayed steps draw nothing: they are not counted as simulated path-steps
 }
 
 // (x_max, stop date) of every path of the chunk -> discounted payoff
