@@ -58,13 +58,13 @@ CONFIGS = {
 DP_OPS_PER_ASSET_STEP = 70.0
 # What the walker actually executes on the fp64 pipe (ncu: DADD+DMUL+DFMA+DSETP
 # thread instructions / executed asset-steps on the C5 label launch of the
-# log-price walker, profiles/r02e/walk_log_c5_sass_mix.txt; the price stepper
+# log-price walker, profiles/r02f/walk_log_c5_sass_mix.txt; the price stepper
 # of the other parity configs executes 80.7): reported beside the algorithmic
 # count, it is fewer because the log-price state needs no per-step exponential.
 DP_OPS_EXECUTED_NCU = 66.3
 DP_OPS_EXECUTED_NCU_PRICE_STEPPER = 80.7
 # DRAM bytes per walker launch from the same capture (dram__bytes_read+write,
-# profiles/r02e/walk_log_c5_summary.txt): label launch 959.7 KB, pricing 80.4 KB
+# profiles/r02f/walk_log_c5_summary.txt): label launch 959.7 KB, pricing 80.4 KB
 WALK_DRAM_BYTES_PER_LAUNCH = (959.7e3 + 80.4e3) / 2
 FP64_LANES_PER_SM = 64
 N_SMS = 148
@@ -304,7 +304,7 @@ def run_engine(args, cfg):
                          "unit": "TFLOP/s" if mode == "parity" else "T thread-instructions/s",
                          "frac": achieved / peak if achieved is not None else None,
                          "asset_steps_per_s": kern_steps * cfg["d"] / (kern_ms / 1e3) if kern_ms > 0 else None,
-                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r02e capture of the C5 walker)",
+                         "traffic": WALK_DRAM_BYTES_PER_LAUNCH, "traffic_unit": "bytes/launch (ncu, r02f capture of the C5 walker)",
                          "kernel": "walk_units+iz_probes",
                          "work": (f"{ops:g} algorithmic " + ("fp64 ops" if mode == "parity" else "thread-instructions")
                                   + " per asset-step (SURVEY.md 8(d)) x executed asset-steps "
@@ -313,6 +313,10 @@ def run_engine(args, cfg):
                          "pipe_utilisation": (achieved * executed / ops / peak) if achieved is not None else None,
                          "kernel_ms_per_step": kern_ms / max(args.steps, 1),
                          "launches_per_step": kern_launches / max(args.steps, 1),
+                         **({"note": "geometric-put probes: only pass 0 of each date's bisection simulates paths "
+                                     "(and is counted); the other passes replay its record (draw cache), so the "
+                                     "fp64 fraction understates the probe kernel by construction"}
+                            if cfg["method"] == "iz" and cfg.get("payoff") == "geoput" and mode == "parity" else {}),
                          "peak_source": "of NOMINAL peak: 148 SM x " + ("64 fp64 lanes" if mode == "parity" else
                                                                 "4 schedulers x 32 lanes") + " x sampled SM clock "
                                         "(MEASURED_PEAKS.json has no fp64 / issue figure)"},
