@@ -347,12 +347,17 @@ int run_walk(brm_ctx *c, Call &call, const WalkJob &j) {
   if (c->hdr.rule == BRM_RULE_CMC && !P.normals && even_ok) {
     // parity mode walks log-prices (brm_walk_log.cuh); BRM_WALK_LOG=0 keeps the price stepper (A/B runs)
     static const bool log_walk = !(std::getenv("BRM_WALK_LOG") && std::getenv("BRM_WALK_LOG")[0] == '0');
+    // BRM_WALK_COLCONST=0 keeps the triangular product for a column-constant factor (A/B runs)
+    static const bool no_colconst = std::getenv("BRM_WALK_COLCONST") && std::getenv("BRM_WALK_COLCONST")[0] == '0';
     const bool maxcall_unit = c->hdr.unit_diag && c->hdr.payoff == BRM_PAY_MAXCALL;
     if (maxcall_unit && !c->fast() && log_walk && c->kern.walk_cmc_log && c->hdr.n_dates <= 255) {
       kwalk = c->kern.walk_cmc_log;
       P.vals_offset = log_model_smem_bytes(c->hdr);  // search trees instead of the bucket tables
     } else if (maxcall_unit && c->kern.walk_cmc_unit) {
       kwalk = c->kern.walk_cmc_unit;
+    } else if (c->fast() && c->hdr.chol_lower == 1 && c->hdr.chol_colconst && c->kern.walk_cmc_colconst &&
+               !no_colconst) {
+      kwalk = c->kern.walk_cmc_colconst;
     } else if (c->fast() && c->hdr.chol_lower == 1 && c->kern.walk_cmc_lower) {
       kwalk = c->kern.walk_cmc_lower;
     } else if (c->kern.walk_cmc) {
@@ -509,6 +514,12 @@ int ctx_create_impl(const brm_market_desc *mk, const brm_rule_desc *rl, int32_t 
   h.unit_diag = diag;
   for (int i = 0; i < d; ++i)
     if (chol[i * d + i] != 1.0) h.unit_diag = 0;
+  // column-constant below the diagonal in the fp32 image the fast walkers read
+  // (the factor of an equicorrelated matrix): fast_step_colconst's prefix form
+  h.chol_colconst = (lower && !diag && d > 2) ? 1 : 0;
+  for (int a = 0; a + 2 < d && h.chol_colconst; ++a)
+    for (int i = a + 2; i < d; ++i)
+      if ((float)chol[i * d + a] != (float)chol[(a + 1) * d + a]) h.chol_colconst = 0;
   std::vector<double> dbl;
   auto put = [&](const std::vector<double> &v, size_t min_len) {
     int off = (int)dbl.size();

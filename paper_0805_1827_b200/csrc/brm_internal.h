@@ -116,6 +116,7 @@ struct KernelTriple {
   void *walk_cmc_log = nullptr;   // ... walk_cmc_unit's case in parity mode on log-prices (brm_walk_log.cuh)
   void *iz_geo_log = nullptr;     // iz_geo on log-prices (log-space surface, independent assets; brm_walk_log.cuh)
   void *iz_geo_log_rec = nullptr; // ... with the bisection draw cache (first pass records, the others replay)
+  void *walk_cmc_colconst = nullptr;  // walk_cmc_lower with a column-constant factor (equicorrelated assets)
 };
 
 // Kernel families for launch accounting (brm_prof.cu, BRM_PROF_* in the C ABI).

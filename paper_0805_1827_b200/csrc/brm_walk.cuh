@@ -99,7 +99,10 @@ __device__ __forceinline__ double geo_payoff(const Model<double> &M, const doubl
 // WALK_CMC_LOWER: fast mode, CMC rule, lower-triangular factor (C4);
 // WALK_CMC_LOG: WALK_CMC_UNIT's case in parity mode with the state kept as
 // log-prices (brm_walk_log.cuh).
-enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_CMC = 2, WALK_CMC_UNIT = 3, WALK_CMC_LOWER = 4, WALK_CMC_LOG = 5 };
+// WALK_CMC_COLCONST: WALK_CMC_LOWER's case with a column-constant factor
+// (fast_step_colconst, brm_model.cuh): equicorrelated assets (C4).
+enum { WALK_GENERIC = 0, WALK_GEO = 1, WALK_CMC = 2, WALK_CMC_UNIT = 3, WALK_CMC_LOWER = 4, WALK_CMC_LOG = 5,
+       WALK_CMC_COLCONST = 6 };
 
 template <int D, bool FAST, int SPEC = WALK_GENERIC>
 __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_start, int m_start, int n_steps,
@@ -130,13 +133,17 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
     // draws are generated by the whole warp (the tail pass is warp-cooperative);
     // lanes without a path draw at a valid dummy index and discard the result
     constexpr bool kFused = FAST && D > 0;
-    const bool fused = kFused && !ns.ptr && M.chol_lower != 0;  // full (non-triangular) factor: generic step
+    // full (non-triangular) factor: generic step
+    const bool fused = kFused && !ns.ptr && (M.chol_lower != 0 || SPEC == WALK_CMC_COLCONST);
     // the CMC instances are launched only with even draw bases (host check)
-    constexpr bool kCmc = SPEC == WALK_CMC || SPEC == WALK_CMC_UNIT || SPEC == WALK_CMC_LOWER;
+    constexpr bool kCmc = SPEC == WALK_CMC || SPEC == WALK_CMC_UNIT || SPEC == WALK_CMC_LOWER ||
+                          SPEC == WALK_CMC_COLCONST;
     if (!fused) path_step_draws<D, FAST, kCmc && D % 2 == 0>(d, K, base, k, ns, z, have, tq);
     if (have) {
       ++nsteps;
-      if constexpr (SPEC == WALK_CMC_LOWER && FAST && D > 0) {
+      if constexpr (SPEC == WALK_CMC_COLCONST && FAST && D > 0) {
+        fast_step_colconst<(D > 0 ? D : 1)>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
+      } else if constexpr (SPEC == WALK_CMC_LOWER && FAST && D > 0) {
         fast_step_fused<(D > 0 ? D : 1), true>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
       } else if constexpr (SPEC == WALK_CMC_UNIT && FAST && D > 0) {
         fast_step_diag<(D > 0 ? D : 1)>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));

@@ -114,3 +114,13 @@ def test_nvtx_range_is_a_noop_without_cuda():
     from paper_0805_1827_b200.engine import nvtx_range
     with nvtx_range("phase"):
         pass
+
+
+def test_column_constant_factor_is_detected_in_fp32_only():
+    """numpy's factor of the equicorrelated matrix is constant below the diagonal only after
+    rounding to fp32 (the fp64 entries differ in the last bits), which is the image the fast
+    walkers read (brm_capi.cu: chol_colconst)."""
+    from tests import _cases as CS
+    L = CS.basketput(40, 20)[0].corr_factor
+    L32 = L.astype(np.float32)
+    assert all(L32[i, a] == L32[a + 1, a] for a in range(38) for i in range(a + 2, 40))
