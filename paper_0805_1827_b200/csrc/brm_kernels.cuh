@@ -42,6 +42,8 @@ __global__ void __launch_bounds__(kWalkThreads, SPEC == WALK_CMC_LOG ? BRM_LOG_M
   __shared__ R s_start[kMaxD];
   __shared__ unsigned char s_stopm[kLog ? kMaxChunk : 1];  // log-price walker: stop date per path slot
   const Model<R> M = load_model<R, kLog>(P.hdr, P.blob, smem);
+  [[maybe_unused]] const float4 *cc_rows = nullptr;
+  if constexpr (SPEC == WALK_CMC_COLCONST) cc_rows = pack_colconst_rows<D>(M);
   double *vals = reinterpret_cast<double *>(smem + P.vals_offset);
   const int d = M.d;
   [[maybe_unused]] const double log_strike = kLog ? log(P.hdr.strike) : 0.0;
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(kWalkThreads, SPEC == WALK_CMC_LOG ? BRM_LOG_M
         finish_log_values(M, P.m_start, p0, p1 - p0, vals, s_stopm, pout, sout);
       } else
         walk_paths<D, FAST, SPEC>(M, s_start, P.m_start, P.n_steps, key, stream, base0, p0, p1, ns, vals, &s_next, pout,
-                                  sout, P.steps, tq);
+                                  sout, P.steps, tq, cc_rows);
     }
     __syncthreads();
     double s = 0.0, q = 0.0;

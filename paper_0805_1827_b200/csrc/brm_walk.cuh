@@ -108,7 +108,8 @@ template <int D, bool FAST, int SPEC = WALK_GENERIC>
 __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_start, int m_start, int n_steps,
                            uint64_t key, uint64_t stream, uint64_t base0, int p0, int p1, const NormalSrc &ns,
                            double *vals, int *s_next, double *path_out, int32_t *stop_out,
-                           unsigned long long *step_count, const TailQueue &tq) {
+                           unsigned long long *step_count, const TailQueue &tq,
+                           [[maybe_unused]] const float4 *cc_rows = nullptr) {
   using R = RealT<FAST>;
   const int d = dim_of<D>(M.d);
   const uint64_t stride = path_stride<FAST>(d, n_steps, ns.ptr != nullptr);
@@ -134,7 +135,7 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
     // lanes without a path draw at a valid dummy index and discard the result
     constexpr bool kFused = FAST && D > 0;
     // full (non-triangular) factor: generic step
-    const bool fused = kFused && !ns.ptr && (M.chol_lower != 0 || SPEC == WALK_CMC_COLCONST);
+    const bool fused = SPEC == WALK_CMC_COLCONST || (kFused && !ns.ptr && M.chol_lower != 0);
     // the CMC instances are launched only with even draw bases (host check)
     constexpr bool kCmc = SPEC == WALK_CMC || SPEC == WALK_CMC_UNIT || SPEC == WALK_CMC_LOWER ||
                           SPEC == WALK_CMC_COLCONST;
@@ -142,7 +143,7 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
     if (have) {
       ++nsteps;
       if constexpr (SPEC == WALK_CMC_COLCONST && FAST && D > 0) {
-        fast_step_colconst<(D > 0 ? D : 1)>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
+        fast_step_colconst<(D > 0 ? D : 1)>(cc_rows, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
       } else if constexpr (SPEC == WALK_CMC_LOWER && FAST && D > 0) {
         fast_step_fused<(D > 0 ? D : 1), true>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
       } else if constexpr (SPEC == WALK_CMC_UNIT && FAST && D > 0) {
