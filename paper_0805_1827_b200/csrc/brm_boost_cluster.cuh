@@ -28,7 +28,10 @@
 
 namespace brm {
 
-constexpr int kCbThreads = 256;
+#ifndef BRM_CB_THREADS
+#define BRM_CB_THREADS 256  // variant builds time other CTA sizes (tools/build_variant.sh)
+#endif
+constexpr int kCbThreads = BRM_CB_THREADS;
 constexpr int kCbQ = 8;                      // sorted positions per thread per tile
 constexpr int kCbBlock = kCbThreads * kCbQ;  // positions per CTA per cluster tile
 constexpr int kCbEvents = 512;               // events per chain per cluster tile (else serial)
@@ -729,10 +732,14 @@ inline size_t cb_smem_bytes(int L, int n_children, int n_levels, int slice_cap, 
 // BRM_MODE_FAST AdaBoost on the same cluster layout: the split search scans
 // weights quantised to 62-bit fixed point (W_i = rint(w_i / s 2^62)), so every
 // prefix is an exact integer scan -- no events, no walker -- and the result
-// is identical for any schedule.  The weight sum s is numpy's pairwise order
-// over the leaves (every CTA combines the same leaf sums), so it does not
-// depend on the cluster size.  Statistically equivalent to the reference,
-// not bit-identical to numpy (tests/test_gpu_config_parity.py, fast mode).
+// is identical for any schedule.  The first weight sum s is numpy's pairwise
+// order over the leaves (every CTA combines the same leaf sums); after a round
+// the reweighted weights sum to e^-a (1 - err) + e^a err with err the winner's
+// error over the quantised weights, so every CTA forms the next s from the
+// integers it already holds -- no pass over the weights, no leaf exchange --
+// and the fit does not depend on the cluster size.  Statistically equivalent
+// to the reference, not bit-identical to numpy
+// (tests/test_gpu_config_parity.py, fast mode).
 constexpr double kFixC = 4611686018427387904.0;  // 2^62
 
 struct CbFastCand {
@@ -750,6 +757,9 @@ __global__ void __launch_bounds__(kCbThreads, 1) boost_fast_cluster_kernel(CbPar
   __shared__ double s_cthr[2];
   __shared__ int s_stop, s_feat;
   __shared__ double s_alpha, s_thr, s_pol, s_err;
+  __shared__ double s_eag, s_emi, s_sum;  // exp(-alpha), exp(alpha), the reweighted weights' sum
+  __shared__ long long s_be;
+  __shared__ int s_bf;
 
   const int n = P.n, F = P.F, cl = P.cl;
   const int r = (int)cluster.block_rank();
@@ -763,7 +773,6 @@ __global__ void __launch_bounds__(kCbThreads, 1) boost_fast_cluster_kernel(CbPar
   const int n_tiles = (n + ctile - 1) / ctile;
   double *s_node = reinterpret_cast<double *>(smem_raw);
   double *s_leaf = s_node + 2 * L;
-  double *s_leaf_b = s_leaf + L;
   double *wsl = s_leaf + 2 * L;
   unsigned *s_code = reinterpret_cast<unsigned *>(wsl + P.slice_cap);
   signed char *s_y = reinterpret_cast<signed char *>(s_code + P.pos_cap);
@@ -858,7 +867,8 @@ __global__ void __launch_bounds__(kCbThreads, 1) boost_fast_cluster_kernel(CbPar
       }
       carry_p += ap;
       carry_n += an;
-      cluster.sync();  // tot_l is reused by the next tile
+      // tot_l is reused by the next tile (after the last one, the next write is a grid barrier away)
+      if (t0 + ctile < n) cluster.sync();
     }
     const long long tot_pos = carry_p, tot_neg = carry_n, total = tot_pos + tot_neg;
 #pragma unroll
@@ -906,23 +916,40 @@ __global__ void __launch_bounds__(kCbThreads, 1) boost_fast_cluster_kernel(CbPar
       P.feat_thr[(round & 1) * F + f] = thr;
     }
     grid.sync();
-    // ---- the winner (every CTA, same answer) -----------------------------
-    if (threadIdx.x == 0) {
+    // ---- the winner (every CTA, same answer): lowest error, lowest feature at equal error ----
+    if (threadIdx.x < 32) {
       const long long *ferr = P.feat_ierr + (round & 1) * F;
-      long long be = LLONG_MAX;
-      int bf = -1, bk = 0;
-      double bt = 0.0;
-      for (int g = 0; g < F; ++g) {
-        const int pos = __ldcg(P.feat_pos + (round & 1) * F + g);
-        const long long e = __ldcg(ferr + g);
-        if (pos != INT_MAX && e < be) be = e, bf = g, bk = pos, bt = __ldcg(P.feat_thr + (round & 1) * F + g);
+      long long e = LLONG_MAX;
+      int g = INT_MAX;
+      for (int q = threadIdx.x; q < F; q += 32) {
+        const long long eq = __ldcg(ferr + q);
+        if (__ldcg(P.feat_pos + (round & 1) * F + q) != INT_MAX && eq < e) e = eq, g = q;
       }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const long long oe = __shfl_down_sync(0xffffffffu, e, off);
+        const int og = __shfl_down_sync(0xffffffffu, g, off);
+        if (og != INT_MAX && (g == INT_MAX || oe < e || (oe == e && og < g))) e = oe, g = og;
+      }
+      if (threadIdx.x == 0) s_be = e, s_bf = g == INT_MAX ? -1 : g;
+    }
+    if (threadIdx.x == 0) {
+      const long long be = s_be;
+      const int bf = s_bf;
+      int bk = 0;
+      double bt = 0.0;
+      if (bf >= 0) {
+        bk = __ldcg(P.feat_pos + (round & 1) * F + bf);
+        bt = __ldcg(P.feat_thr + (round & 1) * F + bf);
+      }
+      long long miss = be;  // fixed-point weight of the misclassified samples
       if (bf < 0) {  // every feature constant: majority constant stump
         const double pol = 2 * tot_neg <= total ? 1.0 : -1.0;  // +1 iff sum(w y) >= 0
         s_feat = 0;
         s_thr = __longlong_as_double(0xfff0000000000000LL);
         s_pol = pol;
-        s_err = (double)(pol > 0 ? tot_neg : total - tot_neg) / (double)total;
+        miss = pol > 0 ? tot_neg : total - tot_neg;
+        s_err = (double)miss / (double)total;
       } else {
         s_feat = bf;
         s_thr = bt;
@@ -941,6 +968,11 @@ __global__ void __launch_bounds__(kCbThreads, 1) boost_fast_cluster_kernel(CbPar
       } else {
         const double a = 0.5 * log((1.0 - err) / (err > 1e-10 ? err : 1e-10));
         s_alpha = a;
+        // the reweighted weights sum to e^-a (1 - err) + e^a err, err over the quantised weights
+        // the split was searched on: known here, so no pass over the weights forms it
+        const double eag = exp(-a), emi = exp(a);
+        s_eag = eag, s_emi = emi;
+        s_sum = (eag * (double)(total - miss) + emi * (double)miss) / (double)total;
         if (blockIdx.x == 0) {
           P.out_feat[count] = s_feat, P.out_thr[count] = s_thr, P.out_pol[count] = s_pol;
           P.out_alpha[count] = a, P.out_err[count] = err;
@@ -952,20 +984,16 @@ __global__ void __launch_bounds__(kCbThreads, 1) boost_fast_cluster_kernel(CbPar
     if (s_stop == 1) break;
     ++count;
     if (s_stop == 3 || round + 1 == P.rounds) break;
-    // ---- reweight this CTA's leaf run; new pairwise sum ---------------------
+    // ---- reweight this CTA's slice (the other CTAs gather it over DSMEM next round) ----------
     {
-      const double a = s_alpha, thr = s_thr, pol = s_pol;
+      const double thr = s_thr, pol = s_pol, e_agree = s_eag, e_miss = s_emi;
       const double *xcol = P.xt + (size_t)s_feat * n;
-      const double e_agree = exp(-a), e_miss = exp(a);
-      double *buf = (round & 1) ? s_leaf : s_leaf_b;  // alternate the leaf-sum buffers (see cb_tree)
-      pw_leaf_sums(
-          T, wloc, l_lo, l_hi, buf,
-          [&](int i, double x) {
-            const double pred = __ldg(xcol + i) > thr ? pol : -pol;
-            return x * inv_s * (((double)s_y[i - e_lo] * pred > 0.0) ? e_agree : e_miss);
-          },
-          [&](int i, double v) { wloc[i] = v; });
-      ssum = cb_tree(cluster, T, buf, s_node, cl);
+      for (int i = e_lo + (int)threadIdx.x; i < e_hi; i += blockDim.x) {
+        const double pred = __ldg(xcol + i) > thr ? pol : -pol;
+        wloc[i] = wloc[i] * inv_s * (((double)s_y[i - e_lo] * pred > 0.0) ? e_agree : e_miss);
+      }
+      ssum = s_sum;
+      cluster.sync();
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) write_result(count, n, n_pos_all, P.out_count, P.out_intercept);
