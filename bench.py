@@ -75,6 +75,9 @@ N_SMS = 148
 # per clock.  The d = 10 walker executes 72.8 (ncu, profiles/r01d_walk_c5_fast.txt).
 FAST_INST_PER_ASSET_STEP = 31.0
 FAST_INST_EXECUTED_NCU_D10 = 72.8
+# d = 40 walker with the column-constant prefix step and the lean Box-Muller / ex2 arithmetic
+# (C4 label launch of date 1, profiles/r02h/walk_c4_fast_lines.txt; 74.0 with the triangular product)
+FAST_INST_EXECUTED_NCU_D40 = 35.2
 ISSUE_LANES_PER_SM = 128
 
 
@@ -270,7 +273,7 @@ def run_engine(args, cfg):
     ops = DP_OPS_PER_ASSET_STEP if mode == "parity" else FAST_INST_PER_ASSET_STEP
     log_walker = cfg["method"] == "cmc" and cfg.get("payoff") == "maxcall" and not cfg.get("rho")
     executed = ((DP_OPS_EXECUTED_NCU if log_walker else DP_OPS_EXECUTED_NCU_PRICE_STEPPER) if mode == "parity"
-                else FAST_INST_EXECUTED_NCU_D10)
+                else (FAST_INST_EXECUTED_NCU_D40 if cfg["d"] == 40 else FAST_INST_EXECUTED_NCU_D10))
     achieved = (kern_steps * cfg["d"] * ops) / (kern_ms / 1e3) / 1e12 if kern_ms > 0 else None
     total_launches = sum(v[1] for v in prof.values())
     total_kernel_ms = sum(v[0] for v in prof.values())
