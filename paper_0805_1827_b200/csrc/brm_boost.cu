@@ -693,7 +693,10 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       // cooperative grid stays co-resident (one cluster per feature)
       int sms = 148;
       BCU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-      int cl = std::max(1, std::min(kCbMaxCluster, sms / F));
+      // fast mode with more features than SMs / 8: the two-CTAs-per-SM instance (wider clusters)
+      const bool two_per_sm = mode == BRM_MODE_FAST && F * kCbMaxCluster > sms;
+      const int slots = two_per_sm ? 2 * sms : sms;
+      int cl = std::max(1, std::min(kCbMaxCluster, slots / F));
       // BRM_NCU_SAFE: one CTA per feature, no cluster launch attribute (Nsight
       // Compute cannot replay cooperative cluster launches); same results
       const bool ncu_safe = getenv("BRM_NCU_SAFE") != nullptr;
@@ -720,13 +723,15 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       BCU(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
       int slice_cap = 0, pos_cap = 0;
       size_t dyn = layout(cl, slice_cap, pos_cap);
-      while (cl < kCbMaxCluster && cl * 2 <= sms / F && dyn + sizeof(CbShared) + 2048 > (size_t)smem_max)
+      while (cl < kCbMaxCluster && cl * 2 <= slots / F && dyn + sizeof(CbShared) + 2048 > (size_t)smem_max)
         dyn = layout(++cl, slice_cap, pos_cap);  // (more CTAs -> smaller slices)
       if (dyn + sizeof(CbShared) + 2048 > (size_t)smem_max) {
         rc = bfail(BRM_EINVAL, "training set too large for the device AdaBoost's shared memory");
         goto done;
       }
-      void *kfn = mode == BRM_MODE_FAST ? (void *)boost_fast_cluster_kernel : (void *)boost_cluster_kernel;
+      void *kfn = mode == BRM_MODE_FAST ? (two_per_sm ? (void *)boost_fast_cluster_kernel<2>
+                                                      : (void *)boost_fast_cluster_kernel<1>)
+                                        : (void *)boost_cluster_kernel;
       BCU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
       cudaLaunchConfig_t lc{};
       cudaLaunchAttribute at[2];
@@ -767,8 +772,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
         void *args[] = {&P};
         const int tok = prof_begin(PK_BOOST, s);
         // fast mode: the same cluster layout with fixed-point integer scans
-        BCU(cudaLaunchKernelExC(&lc, mode == BRM_MODE_FAST ? (void *)boost_fast_cluster_kernel
-                                                            : (void *)boost_cluster_kernel, args));
+        BCU(cudaLaunchKernelExC(&lc, kfn, args));
         prof_end(tok, s);
       }
       if (timing) {

@@ -747,7 +747,11 @@ struct CbFastCand {
   int kmin, kmax;
 };
 
-__global__ void __launch_bounds__(kCbThreads, 1) boost_fast_cluster_kernel(CbParams P) {
+// MINB = 2 (many features, C4: F > SMs / 8): two CTAs per SM, so a feature's cluster is twice as
+// wide and a round covers the sorted positions in half as many tiles; MINB = 1 elsewhere (the
+// 128-register cap costs the small fits 2-4%).
+template <int MINB>
+__global__ void __launch_bounds__(kCbThreads, MINB) boost_fast_cluster_kernel(CbParams P) {
   cg::grid_group grid = cg::this_grid();
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(kWalkThreads, SPEC == WALK_CMC_LOG ? BRM_LOG_M
   const Model<R> M = load_model<R, kLog>(P.hdr, P.blob, smem);
   [[maybe_unused]] const float4 *cc_rows = nullptr;
   if constexpr (SPEC == WALK_CMC_COLCONST) cc_rows = pack_colconst_rows<D>(M);
+  if constexpr (SPEC == WALK_CMC_UNIT && FAST && D > 1)
+    cc_rows = reinterpret_cast<const float4 *>(pack_unit_rows<D>(M));
   double *vals = reinterpret_cast<double *>(smem + P.vals_offset);
   const int d = M.d;
   [[maybe_unused]] const double log_strike = kLog ? log(P.hdr.strike) : 0.0;

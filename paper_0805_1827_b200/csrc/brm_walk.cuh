@@ -146,6 +146,9 @@ __device__ void walk_paths(const Model<RealT<FAST>> &M, const RealT<FAST> *s_sta
         fast_step_colconst<(D > 0 ? D : 1)>(cc_rows, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
       } else if constexpr (SPEC == WALK_CMC_LOWER && FAST && D > 0) {
         fast_step_fused<(D > 0 ? D : 1), true>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
+      } else if constexpr (SPEC == WALK_CMC_UNIT && FAST && D > 1) {
+        fast_step_unit<(D > 1 ? D : 2)>(reinterpret_cast<const float2 *>(cc_rows), v, K,
+                                        base + (uint64_t)k * (uint64_t)fast_dp(D));
       } else if constexpr (SPEC == WALK_CMC_UNIT && FAST && D > 0) {
         fast_step_diag<(D > 0 ? D : 1)>(M, v, K, base + (uint64_t)k * (uint64_t)fast_dp(D));
       } else if constexpr (SPEC == WALK_CMC_UNIT && !FAST) {

@@ -1,6 +1,6 @@
 # fast-mode AdaBoost after the analytic weight sum: timing, the fast-mode tests, C3 / C4 / C5 benches
 set -x
-O=gpurun_out/r02i; mkdir -p $O
+O=gpurun_out/r02j; mkdir -p $O
 for a in "5000 6 150 fast" "10000 11 100 fast" "20000 41 200 fast" "10000 11 100 parity"; do python tools/boost_timing.py $a 2>&1 | tail -1; done > $O/boost_timing.log 2>&1
 cat $O/boost_timing.log
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "tests rc=$?" >> $O/gpu_tests.log
