@@ -226,6 +226,16 @@ int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, void *stream, 
                      int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha, double *out_err,
                      int32_t *out_count, double *out_intercept, int32_t *out_n_pos);
 
+/* Column sort of a DEVICE feature matrix ahead of its fit, ordered on `stream`
+ * (any stream): a later brm_fit_ensemble on the same xs / n / F waits for it
+ * and skips its own transpose and sort -- same sorted columns, same stumps.
+ * brm_ctx_set_presort(ctx, 1) makes brm_cmc_calc do this for the points it
+ * samples, on a high-priority side stream beside the label walk (the sort
+ * needs only the features, boundary_cmc.py:264-271).  An unused sort is
+ * dropped by the next presort of that matrix (at most 4 are kept). */
+int brm_fit_presort(int32_t device, void *stream, const double *xs, int64_t n, int32_t F);
+int brm_ctx_set_presort(brm_ctx *ctx, int32_t on);
+
 /* ---- Device-resident I&Z date step (boundary_iz.py:328-357) ------------- */
 /* Fit date m's boundary surface(s) on the device and write them into the
  * context's rule image, ordered on the context's stream (no host round trip:

@@ -77,6 +77,8 @@ _SIGNATURES = {
                                C.c_void_p]),
     "brm_cmc_calc": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int32,
                                C.c_void_p, C.c_void_p, C.c_void_p]),
+    "brm_fit_presort": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),
+    "brm_ctx_set_presort": (C.c_int, [C.c_void_p, C.c_int32]),
     "brm_fit_ensemble": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import json
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -217,6 +218,10 @@ def _build_device_loop(params, spec, cfg, seed, sampler, mode, shard, torch, str
             feats = torch.empty((rows, F), dtype=f64, device="cuda")
             betas = torch.empty((rows,), dtype=f64, device="cuda")
             off = 0
+            # one rank, one range: the fit below reads this very tensor, so its column sort can run
+            # beside the label walk (brm_fit_presort); BRM_NO_PRESORT=1 keeps it inside the fit
+            ctx.set_presort(not shard.distributed and len(ranges) == 1 and rows == cfg.n_train
+                            and not os.environ.get("BRM_NO_PRESORT"))
             for lo, hi in ranges:
                 if hi > lo:
                     _be.cmc_calc(mp, None, m, seed, lo, hi - lo, cfg.n_label, bridge_scalars(params, spec, m),

@@ -97,6 +97,11 @@ class Context:
         from .packs import RulePack
         return cls(mp, RulePack.european(call_like), device, mode, capacity=capacity)
 
+    def set_presort(self, on: bool) -> None:
+        """brm_cmc_calc sorts the sampled points' feature columns on a side stream beside the label
+        walk, for the fit_ensemble_device call on the same feature tensor that follows."""
+        N.check(N.lib.brm_ctx_set_presort(self.handle, 1 if on else 0))
+
     def set_ensemble(self, m: int, feat, thr, pol, alpha, count, intercept) -> None:
         """Write date m's ensemble (device tensors sized [capacity], count and
         intercept as 1-element tensors) into the image, on the context's stream."""

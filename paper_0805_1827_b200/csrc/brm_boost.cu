@@ -29,6 +29,7 @@
 #include <functional>
 #include <cmath>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/bermuda_b200.h"
@@ -520,6 +521,111 @@ struct Scratch {
 };
 }  // namespace
 
+namespace {
+// Column sorts enqueued ahead of their fit (brm_fit_presort): keyed by the
+// feature matrix they sorted; brm_fit_ensemble on the same matrix takes the
+// entry instead of transposing and sorting again.
+struct Presort {
+  int device;
+  const double *xs;
+  int n, F;
+  double *xt, *xsorted;
+  int *order;
+  cudaEvent_t ready;
+};
+std::mutex g_ps_mu;
+std::vector<Presort> g_ps;
+constexpr size_t kPresortCap = 4;
+
+void presort_release(const Presort &e, cudaStream_t s) {
+  cudaFreeAsync(e.xt, s);
+  cudaFreeAsync(e.xsorted, s);
+  cudaFreeAsync(e.order, s);
+  cudaEventDestroy(e.ready);
+}
+
+bool presort_take(int device, const double *xs, int n, int F, Presort *out) {
+  std::lock_guard<std::mutex> lk(g_ps_mu);
+  for (size_t i = 0; i < g_ps.size(); ++i)
+    if (g_ps[i].device == device && g_ps[i].xs == xs && g_ps[i].n == n && g_ps[i].F == F) {
+      *out = g_ps[i];
+      g_ps.erase(g_ps.begin() + (long)i);
+      return true;
+    }
+  return false;
+}
+}  // namespace
+
+namespace brm {
+int fit_presort(int32_t device, cudaStream_t s, const double *xs, int64_t n64, int32_t F, cudaEvent_t mid);
+}
+extern "C" int brm_fit_presort(int32_t device, void *stream, const double *xs, int64_t n64, int32_t F) {
+  return brm::fit_presort(device, static_cast<cudaStream_t>(stream), xs, n64, F, nullptr);
+}
+
+// mid (optional): recorded between the transpose and the sort, so that a caller can hold its own
+// next kernel until the sort is the next thing the side stream launches
+int brm::fit_presort(int32_t device, cudaStream_t s, const double *xs, int64_t n64, int32_t F, cudaEvent_t mid) {
+  if (!xs || !is_dev(xs)) return bfail(BRM_EINVAL, "brm_fit_presort needs a device feature matrix");
+  if (n64 < 1 || n64 > (int64_t)kCodeId || F < 1 || F > 148 || n64 * F > (int64_t)INT_MAX)
+    return bfail(BRM_EINVAL, "training set size out of range");
+  const int n = (int)n64;
+  int rc = BRM_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  retain_pool(device);
+  Presort e{device, xs, n, F, nullptr, nullptr, nullptr, nullptr};
+  {
+    Presort stale;
+    while (presort_take(device, xs, n, F, &stale)) presort_release(stale, s);  // a sort of this matrix nobody used
+    Scratch S(s);
+    int *d_iota;
+    unsigned long long *k0, *k1;
+    unsigned *i0, *i1;
+    BCU(cudaMallocAsync((void **)&e.xt, sizeof(double) * (size_t)n * F, s));
+    BCU(cudaMallocAsync((void **)&e.xsorted, sizeof(double) * (size_t)n * F, s));
+    BCU(cudaMallocAsync((void **)&e.order, sizeof(int) * (size_t)n * F, s));
+    BCU(S.get(&d_iota, (size_t)n * F));
+    BCU(S.get(&k0, (size_t)n * F));
+    BCU(S.get(&k1, (size_t)n * F));
+    BCU(S.get(&i0, (size_t)n * F));
+    BCU(S.get(&i1, (size_t)n * F));
+    {
+      const int tok = prof_begin(PK_AUX, s);
+      transpose_cols<<<(unsigned)(((int64_t)n * F + 255) / 256), 256, 0, s>>>(xs, n, F, e.xt, d_iota);
+      prof_end(tok, s);
+    }
+    if (mid) BCU(cudaEventRecord(mid, s));
+    {
+      const int tok = prof_begin(PK_AUX, s);
+      sort_columns<<<F, kSortThreads, 0, s>>>(e.xt, n, k0, i0, k1, i1, e.xsorted, e.order);
+      prof_end(tok, s);
+    }
+    BCU(cudaGetLastError());
+    BCU(cudaEventCreateWithFlags(&e.ready, cudaEventDisableTiming));
+    BCU(cudaEventRecord(e.ready, s));
+    {
+      std::lock_guard<std::mutex> lk(g_ps_mu);
+      while (g_ps.size() >= kPresortCap) {  // bounded: drop the oldest unused sort
+        presort_release(g_ps.front(), s);
+        g_ps.erase(g_ps.begin());
+      }
+      g_ps.push_back(e);
+    }
+    e = Presort{};
+  }
+done:
+  if (rc != BRM_OK) {
+    if (e.xt) cudaFreeAsync(e.xt, s);
+    if (e.xsorted) cudaFreeAsync(e.xsorted, s);
+    if (e.order) cudaFreeAsync(e.order, s);
+    if (e.ready) cudaEventDestroy(e.ready);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  return rc;
+}
+
 extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, void *stream, const double *xs,
                                 const double *betas, const double *weights, int64_t n64, int32_t F, int32_t rounds,
                                 int32_t *out_feat, double *out_thr, double *out_pol, double *out_alpha,
@@ -553,8 +659,20 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
     int npos = 0;
     PwTree tree;
     int root = 0;
-    BCU(S.get(&d_xs, (size_t)n * F));
-    BCU(cudaMemcpyAsync(d_xs, xs, sizeof(double) * (size_t)n * F, cudaMemcpyDefault, s));
+    Presort pre{};
+    const bool presorted = presort_take(device, xs, n, F, &pre);
+    if (presorted) {  // sorted ahead on another stream: take its arrays, freed in this call's stream order
+      S.ptrs.push_back(pre.xt);
+      S.ptrs.push_back(pre.xsorted);
+      S.ptrs.push_back(pre.order);
+      const cudaError_t we = cudaStreamWaitEvent(s, pre.ready, 0);
+      cudaEventDestroy(pre.ready);
+      BCU(we);
+      d_xs = nullptr;
+    } else {
+      BCU(S.get(&d_xs, (size_t)n * F));
+      BCU(cudaMemcpyAsync(d_xs, xs, sizeof(double) * (size_t)n * F, cudaMemcpyDefault, s));
+    }
     if (!is_dev(xs)) count_transfer(sizeof(double) * (size_t)n * F, 0);
     if (!is_dev(betas)) count_transfer(sizeof(double) * n, 0);
     BCU(S.get(&d_b, n));
@@ -582,6 +700,11 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       *out_intercept = npos == n ? 1.0 : -1.0;
       goto done;
     }
+    if (presorted) {
+      d_xt = pre.xt;
+      d_xsorted = pre.xsorted;
+      d_order = pre.order;
+    } else {
     BCU(S.get(&d_xt, (size_t)n * F));
     BCU(S.get(&d_xsorted, (size_t)n * F));
     BCU(S.get(&d_iota, (size_t)n * F));
@@ -602,6 +725,7 @@ extern "C" int brm_fit_ensemble(int32_t device, int32_t mode, int32_t flags, voi
       const int tok = prof_begin(PK_AUX, s);
       sort_columns<<<F, kSortThreads, 0, s>>>(d_xt, n, k0, i0, k1, i1, d_xsorted, d_order);
       prof_end(tok, s);
+    }
     }
     BCU(S.get(&d_w, n));
     if (weights) {

@@ -263,6 +263,11 @@ struct brm_ctx {
   double *normals = nullptr;  // supplied-normals copy (device)
   cudaEvent_t ready = nullptr;  // image upload complete (waited on by every launch stream)
   cudaEvent_t retired = nullptr;  // scratch event: work of a stream the context stops using
+  // brm_ctx_set_presort: brm_cmc_calc sorts the feature columns of the points it samples on a
+  // side stream (high priority, beside the label walk), for the brm_fit_ensemble that follows
+  bool presort = false;
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t side_event = nullptr, side_mid = nullptr;
   uint64_t nrm_base = 0, nrm_count = 0;
   int capacity = 0;  // > 0: slotted CMC image (brm_ctx_create_cmc)
   SlotDims slot{};
@@ -800,6 +805,9 @@ int brm_ctx_destroy(brm_ctx *c) {
   if (c->normals) cudaFreeAsync(c->normals, s);
   if (c->ready) cudaEventDestroy(c->ready);
   if (c->retired) cudaEventDestroy(c->retired);
+  if (c->side_event) cudaEventDestroy(c->side_event);
+  if (c->side_mid) cudaEventDestroy(c->side_mid);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);  // (its work completes first)
   cudaGetLastError();
   delete c;
   return BRM_OK;
@@ -1124,6 +1132,12 @@ int brm_sample_points(brm_ctx *c, int32_t mode, int32_t m, uint64_t seed, int64_
   return call.finish();
 }
 
+int brm_ctx_set_presort(brm_ctx *c, int32_t on) {
+  if (!c) return fail(BRM_EINVAL, "NULL context");
+  c->presort = on != 0;
+  return BRM_OK;
+}
+
 int brm_cmc_calc(brm_ctx *c, int32_t sampler, int32_t m, uint64_t seed, int64_t item_lo, int64_t n,
                  int32_t n_label, const double *bridge, double *out_features, double *out_beta) {
   if (!c || !out_features || !out_beta) return fail(BRM_EINVAL, "NULL argument");
@@ -1163,6 +1177,23 @@ int brm_cmc_calc(brm_ctx *c, int32_t sampler, int32_t m, uint64_t seed, int64_t 
     const int tok_ = prof_begin(PK_SAMPLE, call.stream);
     BRM_CUDA(cudaLaunchKernel(sample_kernel(), dim3((unsigned)((n + 127) / 128)), dim3(128), sargs, 0, call.stream));
     prof_end(tok_, call.stream);
+  }
+  if (c->presort && S.out == out_features) {
+    // the features are final once the sampler is done: their column sort (AdaBoost's fixed cost)
+    // runs on a few SMs beside the label walk instead of after it
+    if (!c->side_stream) {
+      int lo_p = 0, hi_p = 0;
+      BRM_CUDA(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+      BRM_CUDA(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, hi_p));
+      BRM_CUDA(cudaEventCreateWithFlags(&c->side_event, cudaEventDisableTiming));
+    }
+    BRM_CUDA(cudaEventRecord(c->side_event, call.stream));
+    BRM_CUDA(cudaStreamWaitEvent(c->side_stream, c->side_event, 0));
+    if (!c->side_mid) BRM_CUDA(cudaEventCreateWithFlags(&c->side_mid, cudaEventDisableTiming));
+    BRM_TRY(fit_presort(c->device, c->side_stream, out_features, n, F, c->side_mid));
+    // the walk starts once the sort is the side stream's next launch: the sort's few CTAs get
+    // their SMs before the walker's persistent CTAs fill the device
+    BRM_CUDA(cudaStreamWaitEvent(call.stream, c->side_mid, 0));
   }
   WalkJob j;
   j.n_units = (int)n;

@@ -200,3 +200,30 @@ def test_partitions_give_identical_bits_at_c2_probe_count():
         assert np.array_equal(coeffs, out[0][0])
         assert its == out[0][1]
         assert p == out[0][2]
+
+
+def test_fit_presort_on_a_side_stream_gives_the_same_ensemble():
+    """brm_fit_presort (the column sort ahead of its fit, on another stream): the fit that finds it
+    returns the stumps of a fit that sorts itself, in both modes; a sort nobody uses is dropped."""
+    import torch
+    from paper_0805_1827_b200 import _native as N
+    from paper_0805_1827_b200 import backend as G
+    rng = np.random.default_rng(12)
+    n, F = 3000, 6
+    X = 100 * np.exp(0.2 * rng.normal(size=(n, F)))
+    X[:, -1] = X[:, :-1].max(axis=1)
+    beta = (X[:, -1] - 125) + 0.4 * (X[:, 0] - 100) + 6 * rng.normal(size=n)
+    xs, bs = torch.from_numpy(X).cuda(), torch.from_numpy(beta).cuda()
+    side = torch.cuda.Stream()
+    for mode in ("parity", "fast"):
+        plain = G.fit_ensemble_arrays(xs, bs, 40, mode=mode)
+        for _ in range(2):  # the first sort is replaced by the second, which the fit takes
+            N.check(N.lib.brm_fit_presort(0, N.stream_handle(side), N.ptr(xs), n, F))
+        pre = G.fit_ensemble_arrays(xs, bs, 40, mode=mode)
+        again = G.fit_ensemble_arrays(xs, bs, 40, mode=mode)  # nothing left to take: sorts itself
+        for a, b, c in zip(plain, pre, again):
+            assert np.array_equal(np.asarray(a), np.asarray(b)) and np.array_equal(np.asarray(a), np.asarray(c))
+    N.check(N.lib.brm_fit_presort(0, N.stream_handle(side), N.ptr(xs), n, F))  # left unused on purpose
+    torch.cuda.synchronize()
+    with pytest.raises(Exception):
+        N.check(N.lib.brm_fit_presort(0, N.stream_handle(side), N.ptr(X), n, F))  # host matrix: refused
