@@ -297,8 +297,12 @@ def build_cmc_rule(params, spec, cfg: CmcBuildConfig, seed: int = 0, engine=None
         if torch is not None:
             # device-resident date step: features and labels stay in HBM, every
             # launch (sampler, walker, AdaBoost) is ordered on torch's stream
-            get_context(mp, later, mode=mode).set_stream(stream)
+            date_ctx = get_context(mp, later, mode=mode)
+            date_ctx.set_stream(stream)
             rows = sum(hi - lo for lo, hi in ranges)
+            # (as in the device loop: the fit's column sort beside the label walk)
+            date_ctx.set_presort(not shard.distributed and len(ranges) == 1 and rows == cfg.n_train
+                                 and not os.environ.get("BRM_NO_PRESORT"))
             feats = torch.empty((rows, F), dtype=torch.float64, device="cuda")
             betas = torch.empty((rows,), dtype=torch.float64, device="cuda")
             off = 0

@@ -532,6 +532,7 @@ struct Presort {
   double *xt, *xsorted;
   int *order;
   cudaEvent_t ready;
+  const void *owner;  // the context whose brm_cmc_calc enqueued it (dropped with the context), or NULL
 };
 std::mutex g_ps_mu;
 std::vector<Presort> g_ps;
@@ -557,15 +558,32 @@ bool presort_take(int device, const double *xs, int n, int F, Presort *out) {
 }  // namespace
 
 namespace brm {
-int fit_presort(int32_t device, cudaStream_t s, const double *xs, int64_t n64, int32_t F, cudaEvent_t mid);
+int fit_presort(int32_t device, cudaStream_t s, const double *xs, int64_t n64, int32_t F, cudaEvent_t mid,
+                const void *owner);
+void fit_presort_drop(const void *owner, cudaStream_t s);
 }
 extern "C" int brm_fit_presort(int32_t device, void *stream, const double *xs, int64_t n64, int32_t F) {
-  return brm::fit_presort(device, static_cast<cudaStream_t>(stream), xs, n64, F, nullptr);
+  return brm::fit_presort(device, static_cast<cudaStream_t>(stream), xs, n64, F, nullptr, nullptr);
+}
+
+// Sorts a context enqueued and no fit took (an exception between brm_cmc_calc and the fit): dropped
+// with the context, so that a later matrix at the same address never meets them.
+void brm::fit_presort_drop(const void *owner, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_ps_mu);
+  for (size_t i = 0; i < g_ps.size();) {
+    if (g_ps[i].owner == owner) {
+      presort_release(g_ps[i], s);
+      g_ps.erase(g_ps.begin() + (long)i);
+    } else {
+      ++i;
+    }
+  }
 }
 
 // mid (optional): recorded between the transpose and the sort, so that a caller can hold its own
 // next kernel until the sort is the next thing the side stream launches
-int brm::fit_presort(int32_t device, cudaStream_t s, const double *xs, int64_t n64, int32_t F, cudaEvent_t mid) {
+int brm::fit_presort(int32_t device, cudaStream_t s, const double *xs, int64_t n64, int32_t F, cudaEvent_t mid,
+                     const void *owner) {
   if (!xs || !is_dev(xs)) return bfail(BRM_EINVAL, "brm_fit_presort needs a device feature matrix");
   if (n64 < 1 || n64 > (int64_t)kCodeId || F < 1 || F > 148 || n64 * F > (int64_t)INT_MAX)
     return bfail(BRM_EINVAL, "training set size out of range");
@@ -575,7 +593,7 @@ int brm::fit_presort(int32_t device, cudaStream_t s, const double *xs, int64_t n
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   retain_pool(device);
-  Presort e{device, xs, n, F, nullptr, nullptr, nullptr, nullptr};
+  Presort e{device, xs, n, F, nullptr, nullptr, nullptr, nullptr, owner};
   {
     Presort stale;
     while (presort_take(device, xs, n, F, &stale)) presort_release(stale, s);  // a sort of this matrix nobody used

@@ -805,6 +805,7 @@ int brm_ctx_destroy(brm_ctx *c) {
   if (c->normals) cudaFreeAsync(c->normals, s);
   if (c->ready) cudaEventDestroy(c->ready);
   if (c->retired) cudaEventDestroy(c->retired);
+  if (c->side_stream) fit_presort_drop(c, c->side_stream);
   if (c->side_event) cudaEventDestroy(c->side_event);
   if (c->side_mid) cudaEventDestroy(c->side_mid);
   if (c->side_stream) cudaStreamDestroy(c->side_stream);  // (its work completes first)
@@ -1190,7 +1191,7 @@ int brm_cmc_calc(brm_ctx *c, int32_t sampler, int32_t m, uint64_t seed, int64_t 
     BRM_CUDA(cudaEventRecord(c->side_event, call.stream));
     BRM_CUDA(cudaStreamWaitEvent(c->side_stream, c->side_event, 0));
     if (!c->side_mid) BRM_CUDA(cudaEventCreateWithFlags(&c->side_mid, cudaEventDisableTiming));
-    BRM_TRY(fit_presort(c->device, c->side_stream, out_features, n, F, c->side_mid));
+    BRM_TRY(fit_presort(c->device, c->side_stream, out_features, n, F, c->side_mid, c));
     // the walk starts once the sort is the side stream's next launch: the sort's few CTAs get
     // their SMs before the walker's persistent CTAs fill the device
     BRM_CUDA(cudaStreamWaitEvent(call.stream, c->side_mid, 0));

@@ -129,7 +129,9 @@ void count_transfer(size_t h2d, size_t d2h);
 
 KernelTriple kernels_for(int d, bool fast);
 // brm_fit_presort with an event recorded between its transpose and its sort (brm_boost.cu)
-int fit_presort(int32_t device, cudaStream_t s, const double *xs, int64_t n, int32_t F, cudaEvent_t mid);
+int fit_presort(int32_t device, cudaStream_t s, const double *xs, int64_t n, int32_t F, cudaEvent_t mid,
+                const void *owner);
+void fit_presort_drop(const void *owner, cudaStream_t s);  // unused sorts of a context being destroyed
 int set_error(int code, const char *fmt, ...);
 void *finish_kernel();
 void *sample_kernel();
