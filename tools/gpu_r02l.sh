@@ -1,8 +1,8 @@
-# Round-2 (k) measurement set, run under gpurun from the repo root: GPU tests, smoke, the five
+# Round-2 (l) measurement set, run under gpurun from the repo root: GPU tests, smoke, the five
 # bench configs, the reference arm, the C5 launch list, the C5 walker's full ncu capture and the
 # C4 walker's (column-constant fast step).
 set -x
-O=gpurun_out/r02k; mkdir -p $O
+O=gpurun_out/r02l; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "tests rc=$?" >> $O/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
